@@ -1,0 +1,230 @@
+/*
+ * glint_b200.h -- C ABI of the B200 (sm_100a) layer-wise GNN inference kernels.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `glint` (arXiv 2211.15082, "DGI").  The reference has no FFI of its own: its
+ * boundary is the Python module API in pkg/src/glint/kernels.py and the
+ * engine in pkg/src/glint/executor.py.  Each entry point below names the
+ * reference interface it replaces (file:line relative to the reference's
+ * pkg/src/glint/).  INTEGRATION.md shows the ctypes binding a glint maintainer
+ * would add.
+ *
+ * Conventions
+ *   - Every pointer argument is caller-allocated DEVICE memory unless the
+ *     comment says "host".  The library never allocates or frees caller
+ *     memory; scratch space is passed in as an explicit workspace whose size
+ *     the matching *_workspace_bytes() query returns.
+ *   - Every launching call takes a stream (a cudaStream_t; NULL = legacy
+ *     default stream) and is asynchronous: no hidden host synchronisation.
+ *   - Return value: 0 on success, a negative GLINT_E* code on failure; the
+ *     message is available from glint_last_error() (thread-local).
+ *     GLINT_EINVAL maps to Python ValueError (the reference kernels raise
+ *     ValueError on shape mismatch, kernels.py:99-105,129-130,180-181);
+ *     GLINT_ECUDA maps to glint.errors.InternalError (errors.py:37-38).
+ *   - Matrices are row-major fp32 with an explicit leading dimension (row
+ *     pitch, in elements).  When ld % 4 == 0 and the base is 16-byte aligned
+ *     the kernels use 128-bit loads; otherwise a scalar path runs.
+ *   - Node ids in adjacency `indices` are int32 on device (111M-node graphs
+ *     fit); offsets (`indptr`) and row-id lists are int64, as in the reference
+ *     (storage.py:47-48).
+ */
+#ifndef GLINT_B200_H
+#define GLINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* glint_stream_t; /* cudaStream_t */
+
+#define GLINT_OK 0
+#define GLINT_EINVAL (-1)
+#define GLINT_ECUDA (-2)
+#define GLINT_EUNSUPPORTED (-3)
+
+/* Elementwise kinds (kernels.py:25 ELEMENTWISE_KINDS order). */
+#define GLINT_EW_RELU 0
+#define GLINT_EW_LEAKY_RELU 1
+#define GLINT_EW_ADD 2
+#define GLINT_EW_NORM 3
+#define GLINT_EW_DROPOUT_IDENTITY 4
+
+/* Epilogue activations fused into glint_linear_f32. */
+#define GLINT_ACT_NONE 0
+#define GLINT_ACT_RELU 1
+#define GLINT_ACT_LEAKY_RELU 2
+
+/* GEMM precisions. */
+#define GLINT_PREC_FP32 0   /* CUDA-core fp32 FMA chain, fixed k order */
+#define GLINT_PREC_3XTF32 1 /* tcgen05 kind::tf32, split operands (big+small), 3 MMAs */
+
+/* ------------------------------------------------------------------ misc */
+const char* glint_last_error(void);
+int glint_abi_version(void);
+/* host pointers; fills the properties of `device` */
+int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                      size_t* free_bytes, size_t* total_bytes);
+
+/* ----------------------------------------------------- K1 mean aggregation
+ * Replaces kernels.py:122-135 agg_mean (and _segment_sum kernels.py:110-115).
+ * For output row r (0 <= r < n_rows):
+ *   rid  = row_ids ? row_ids[r] : row_base + r            (CSR row)
+ *   map(u) = col_map ? col_map[u] : u                      (row of h)
+ *   self = self_rows ? self_rows[r] : map(rid)
+ *   out[r, c] = ((0 + h[map(u_0), c]) + h[map(u_1), c] + ... + h[self, c])
+ *               / (float)(deg + 1)
+ * with u_k = indices[indptr[rid] + k] in STORED order and IEEE fp32 adds /
+ * division -- byte-identical to the reference's np.add.at accumulation.
+ * `schedule` (nullable) is a processing order of the n_rows output rows as
+ * produced by glint_degree_schedule; its first n_hub entries are hub rows
+ * processed cooperatively by a whole CTA (columns split across threads, so
+ * the per-column summation order is unchanged).  Without a schedule rows run
+ * in natural order and n_hub must be 0. */
+int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
+                        const int32_t* indices, const int64_t* row_ids,
+                        int64_t row_base, const int64_t* self_rows,
+                        const int32_t* col_map, const float* h, int64_t ld_h,
+                        float* out, int64_t ld_out, const int32_t* schedule,
+                        int64_t n_hub, glint_stream_t stream);
+
+/* Degree-bucketed longest-first schedule over n_rows output rows (CSR rows
+ * as for glint_spmm_mean_f32).  Writes a permutation of [0, n_rows) to
+ * schedule_out: rows bucketed by floor(log2(deg+1)) in descending bucket
+ * order; *n_hub_out (device int64) = number of leading rows whose
+ * deg + 1 >= hub_min_degree (hub_min_degree must be a power of two, or 0
+ * to disable the hub path). */
+size_t glint_degree_schedule_workspace_bytes(void);
+int glint_degree_schedule(int64_t n_rows, const int64_t* indptr,
+                          const int64_t* row_ids, int64_t row_base,
+                          int64_t hub_min_degree, int32_t* schedule_out,
+                          int64_t* n_hub_out, void* workspace,
+                          size_t workspace_bytes, glint_stream_t stream);
+
+/* ------------------------------------------------------ K2 dense transform
+ * Replaces kernels.py:95-107 linear (einsum "ij,kj->ik" + bias), with an
+ * optional fused activation (elementwise ReLU/LeakyReLU, kernels.py:206-215).
+ *   C[i, n] = act( sum_k A[a_row(i), k] * W[n, k] + bias[n] )
+ * a_rows (nullable) gathers A rows.  Each output row depends only on its own
+ * A row (row/batch invariant, kernels.py:1-14). */
+int glint_linear_f32(int64_t M, int32_t N, int32_t K, const float* A,
+                     int64_t lda, const int64_t* a_rows, const float* W,
+                     int64_t ldw, const float* bias, int32_t act, float* C,
+                     int64_t ldc, int32_t precision, glint_stream_t stream);
+
+/* -------------------------------------------------------- K3/K4 attention
+ * Replaces kernels.py:170-203 agg_attn.  The projection z_h = linear(h, W_h)
+ * for all heads is one glint_linear_f32 into a head-padded Z
+ * (Z[:, h*ldh + j], ldh >= head_dim), then: */
+/* s_src[i,h] = z_h[i] . attn[h, :dh]; s_dst[i,h] = z_h[i] . attn[h, dh:]
+ * (einsum "ij,j->i", kernels.py:188-189). */
+int glint_gat_scores_f32(int64_t M, int32_t heads, int32_t head_dim,
+                         int32_t head_pitch, const float* Z, int64_t ldz,
+                         const float* attn, float* s_src, float* s_dst,
+                         glint_stream_t stream);
+/* Edge softmax + weighted sum over N(v) u {v} per head (kernels.py:190-202):
+ * logit = LeakyReLU_slope(s_src[u,h] + s_dst[v,h]); peak = max(self, edges);
+ * w = exp(logit - peak); out[r, h*head_dim + j] =
+ *   (sum_e w_e * z_h[u_e, j] (stored order) + w_self * z_h[v, j]) /
+ *   (sum_e w_e + w_self).  Row addressing as glint_spmm_mean_f32; the
+ * self row of Z / s_* is `self`, the source rows map(u). */
+int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim,
+                            int32_t head_pitch, const int64_t* indptr,
+                            const int32_t* indices, const int64_t* row_ids,
+                            int64_t row_base, const int64_t* self_rows,
+                            const int32_t* col_map, const float* Z, int64_t ldz,
+                            const float* s_src, const float* s_dst, float slope,
+                            float* out, int64_t ld_out, const int32_t* schedule,
+                            int64_t n_hub, glint_stream_t stream);
+
+/* --------------------------------------------------- K5 per-row operators
+ * Replaces kernels.py:206-231 elementwise.  inputs / ld_inputs / input_rows
+ * are HOST arrays of n_inputs entries (device pointers inside); input_rows[k]
+ * (nullable) gathers rows of operand k (the executor's target restriction,
+ * executor.py:358-368).  Add sums operands sequentially in order. */
+int glint_elementwise_f32(int32_t kind, int64_t n_rows, int32_t dim,
+                          int32_t n_inputs, const float* const* inputs,
+                          const int64_t* ld_inputs,
+                          const int64_t* const* input_rows, float* out,
+                          int64_t ld_out, glint_stream_t stream);
+
+/* Row copy with optional gather/scatter: dst[dst_row(i), :dim] =
+ * src[src_row(i), :dim].  Serves EmbeddingStore.gather/scatter
+ * (storage.py:224-246), concat (kernels.py:234-239, dst column offset via
+ * the dst pointer) and apply_order's feature permutation (reorder.py:175-180). */
+int glint_copy_rows_f32(int64_t n_rows, int32_t dim, const float* src,
+                        int64_t ld_src, const int64_t* src_rows, float* dst,
+                        int64_t ld_dst, const int64_t* dst_rows,
+                        glint_stream_t stream);
+
+/* ------------------------------------------------ K6 integer set machinery
+ * Sorted id sets over [0, num_nodes) as a bitmap plus per-word rank prefix.
+ * Replaces the np.unique / np.searchsorted pairs of build_batch_csc
+ * (kernels.py:71-77), trivial_batch_csc (kernels.py:80-88), _expand
+ * (executor.py:118-121) and _StoreEntry.locate (executor.py:270-276). */
+size_t glint_idset_workspace_bytes(int64_t num_nodes);
+int glint_idset_clear(void* ws, int64_t num_nodes, glint_stream_t stream);
+/* add ids[0..n) (ids == NULL: add the range [base, base+n)) */
+int glint_idset_add_ids(void* ws, int64_t num_nodes, const int64_t* ids,
+                        int64_t base, int64_t n, glint_stream_t stream);
+/* add the in-neighbours of targets (targets == NULL: rows [base, base+n)) */
+int glint_idset_add_neighbors(void* ws, int64_t num_nodes, const int64_t* indptr,
+                              const int32_t* indices, const int64_t* targets,
+                              int64_t base, int64_t n, glint_stream_t stream);
+/* rank prefix; *count_out (device int64) = |set| */
+int glint_idset_finalize(void* ws, int64_t num_nodes, int64_t* count_out,
+                         glint_stream_t stream);
+/* ascending members -> ids_out[0..|set|) (after finalize) */
+int glint_idset_extract(const void* ws, int64_t num_nodes, int64_t* ids_out,
+                        glint_stream_t stream);
+/* pos[i] = rank of ids[i] in the set, -1 when absent (after finalize).
+ * Either output may be NULL. */
+int glint_idset_lookup(const void* ws, int64_t num_nodes, const int64_t* ids,
+                       const int32_t* ids32, int64_t n, int64_t* pos64,
+                       int32_t* pos32, glint_stream_t stream);
+/* dense id -> rank map over all nodes: map[u] = rank or -1 */
+int glint_idset_rank_map(const void* ws, int64_t num_nodes, int32_t* map_out,
+                         glint_stream_t stream);
+
+/* Exclusive prefix of in-degrees over a target list: out[0] = 0,
+ * out[j+1] = out[j] + deg(target_j).  Replaces storage.py:159-165
+ * prefix_for_targets and the local indptr of gather_slices
+ * (kernels.py:56-68).  targets == NULL: rows [base, base+n). */
+size_t glint_scan_workspace_bytes(int64_t n);
+int glint_degree_prefix(const int64_t* indptr, const int64_t* targets,
+                        int64_t base, int64_t n, int64_t* out, void* ws,
+                        size_t ws_bytes, glint_stream_t stream);
+/* Concatenated in-neighbour slices (kernels.py:56-68 gather_slices):
+ * srcs[local_indptr[j] + k] = indices[indptr[t_j] + k]; either output may
+ * be NULL; local positions through an idset when pos_ws != NULL
+ * (local_srcs of build_batch_csc). */
+int glint_gather_slices(const int64_t* indptr, const int32_t* indices,
+                        const int64_t* targets, int64_t base, int64_t n,
+                        const int64_t* local_indptr, int64_t* srcs64,
+                        int32_t* srcs32, const void* pos_ws, int64_t num_nodes,
+                        int64_t* local64, int32_t* local32,
+                        glint_stream_t stream);
+
+/* ------------------------------------------------------ graph utilities */
+/* apply_order relabel (reorder.py:149-181): new row j = old row perm[j],
+ * slice mapped elementwise through inv, stored order preserved. */
+int glint_relabel_csc(int64_t num_nodes, const int64_t* old_indptr,
+                      const int32_t* old_indices, const int64_t* perm,
+                      const int64_t* inv, const int64_t* new_indptr,
+                      int32_t* new_indices, glint_stream_t stream);
+/* int64 -> int32 id narrowing with range check; *bad_out (device int64)
+ * receives the count of ids outside [0, limit). */
+int glint_narrow_ids(int64_t n, const int64_t* src, int32_t* dst,
+                     int64_t limit, int64_t* bad_out, glint_stream_t stream);
+
+/* Host-side (pure C++, host pointers): reverse Cuthill-McKee order with the
+ * reference's tie rules (reorder.py:55-123). perm_out[new] = old. */
+int glint_rcmk_host(int64_t num_nodes, const int64_t* indptr,
+                    const int64_t* indices, int64_t* perm_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLINT_B200_H */

@@ -1,0 +1,650 @@
+// K1 (mean SpMM) and K4 (GAT edge-softmax SpMM) neighbour aggregation.
+//
+// Reference semantics: kernels.py:122-135 (agg_mean) and kernels.py:170-203
+// (agg_attn).  The mean must be byte-identical to numpy's np.add.at
+// accumulation: every output column is ONE sequential fp32 add chain
+//   0 + h[u_0] + h[u_1] + ... + h[u_{deg-1}] + h[self]
+// in stored edge order, followed by an IEEE division by (float)(deg+1).
+// Parallelism therefore comes only from (a) rows, (b) columns and (c) issuing
+// many independent row loads ahead of the in-order adds -- never from a
+// reduction tree over edges.
+//
+// Layout of the work:
+//   * regular rows: a group of LPR lanes (8/16/32) owns one row; each lane
+//     owns VPL 128-bit column chunks; U neighbour rows are loaded ahead of the
+//     adds (memory-level parallelism ~ U*VPL*16 B per lane).
+//   * hub rows (deg+1 >= hub_min, first n_hub entries of the degree-bucketed
+//     schedule): a whole 256-thread CTA owns (row, 256-column block); each
+//     thread owns one column and keeps UH loads in flight, source offsets are
+//     staged in shared memory.  Hub CTAs have the lowest blockIdx so they are
+//     dispatched first (longest-processing-time-first), regular rows follow
+//     in descending degree-bucket order.
+#include <cub/block/block_reduce.cuh>
+
+#include "common.cuh"
+
+namespace glint {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kHubChunk = 1024;  // staged source offsets per hub iteration
+constexpr int kHubUnroll = 32;   // loads in flight per thread on the hub path
+constexpr int kMaxHeads = 8;
+
+struct RowAddr {
+  const int64_t* __restrict__ indptr;
+  const int32_t* __restrict__ indices;
+  const int64_t* __restrict__ row_ids;
+  int64_t row_base;
+  const int64_t* __restrict__ self_rows;
+  const int32_t* __restrict__ col_map;
+
+  __device__ __forceinline__ int64_t csr_row(int64_t r) const {
+    return row_ids ? row_ids[r] : row_base + r;
+  }
+  __device__ __forceinline__ int64_t map(int64_t u) const {
+    return col_map ? static_cast<int64_t>(col_map[u]) : u;
+  }
+  __device__ __forceinline__ int64_t self_row(int64_t r, int64_t rid) const {
+    return self_rows ? self_rows[r] : map(rid);
+  }
+};
+
+struct Sched {
+  const int32_t* __restrict__ schedule;
+  int64_t n_rows;
+  int64_t n_hub;
+  int hub_col_blocks;
+  int64_t hub_ctas;
+};
+
+__device__ __forceinline__ int64_t shfl64(unsigned mask, int64_t v, int src, int width) {
+  int lo = __shfl_sync(mask, static_cast<int>(v & 0xffffffffLL), src, width);
+  int hi = __shfl_sync(mask, static_cast<int>(v >> 32), src, width);
+  return (static_cast<int64_t>(hi) << 32) | static_cast<uint32_t>(lo);
+}
+
+// ------------------------------------------------------------------ mean --
+
+struct MeanArgs {
+  RowAddr ra;
+  Sched sc;
+  int dim;
+  const float* __restrict__ h;
+  int64_t ld_h;
+  float* __restrict__ out;
+  int64_t ld_out;
+};
+
+template <int VEC>
+__device__ __forceinline__ void load_vec(float (&v)[VEC], const float* p) {
+  if constexpr (VEC == 4) {
+    float4 t = ldg_f4(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    v[0] = __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* p, const float (&v)[VEC], int valid) {
+  if constexpr (VEC == 4) {
+    if (valid >= 4) {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int c = 0; c < valid; ++c) p[c] = v[c];
+    }
+  } else {
+    p[0] = v[0];
+  }
+}
+
+template <int VEC, int LPR, int VPL, int U>
+__device__ __forceinline__ void mean_row_regular(const MeanArgs& a, int64_t r, int lane_g,
+                                                 unsigned gmask) {
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self_off = a.ra.self_row(r, rid) * a.ld_h;
+  const float degp1 = static_cast<float>(end - beg + 1);
+  constexpr int TILE = LPR * VPL * VEC;
+
+  for (int c0 = 0; c0 < a.dim; c0 += TILE) {
+    float acc[VPL][VEC];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) acc[k][c] = 0.0f;
+
+    for (int64_t e0 = beg; e0 < end; e0 += LPR) {
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(LPR), end - e0));
+      int64_t my = 0;
+      if (lane_g < cnt) my = a.ra.map(a.ra.indices[e0 + lane_g]) * a.ld_h;
+      for (int j = 0; j < cnt; j += U) {
+        float v[U][VPL][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t off = shfl64(gmask, my, (j + u) & (LPR - 1), LPR);
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const int col = c0 + (lane_g + LPR * k) * VEC;
+            if (j + u < cnt && col < a.dim) {
+              load_vec<VEC>(v[u][k], a.h + off + col);
+            } else {
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) v[u][k][c] = 0.0f;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j + u < cnt) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) acc[k][c] = __fadd_rn(acc[k][c], v[u][k][c]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int col = c0 + (lane_g + LPR * k) * VEC;
+      if (col < a.dim) {
+        float s[VEC];
+        load_vec<VEC>(s, a.h + self_off + col);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc[k][c] = __fdiv_rn(__fadd_rn(acc[k][c], s[c]), degp1);
+        store_vec<VEC>(a.out + r * a.ld_out + col, acc[k], a.dim - col);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void mean_row_hub(const MeanArgs& a, int64_t r, int col_block,
+                                             int64_t* s_off) {
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self_off = a.ra.self_row(r, rid) * a.ld_h;
+  const float degp1 = static_cast<float>(end - beg + 1);
+  const int col = col_block * kThreads + threadIdx.x;
+  const bool active = col < a.dim;
+  float acc = 0.0f;
+  for (int64_t e0 = beg; e0 < end; e0 += kHubChunk) {
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kHubChunk), end - e0));
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kThreads)
+      s_off[t] = a.ra.map(a.ra.indices[e0 + t]) * a.ld_h;
+    __syncthreads();
+    if (active) {
+      for (int j = 0; j < cnt; j += kHubUnroll) {
+        float v[kHubUnroll];
+#pragma unroll
+        for (int u = 0; u < kHubUnroll; ++u)
+          v[u] = (j + u < cnt) ? __ldg(a.h + s_off[j + u] + col) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < kHubUnroll; ++u)
+          if (j + u < cnt) acc = __fadd_rn(acc, v[u]);
+      }
+    }
+  }
+  if (active) {
+    acc = __fadd_rn(acc, __ldg(a.h + self_off + col));
+    a.out[r * a.ld_out + col] = __fdiv_rn(acc, degp1);
+  }
+}
+
+template <int VEC, int LPR, int VPL, int U>
+__global__ void __launch_bounds__(kThreads) mean_kernel(MeanArgs a) {
+  __shared__ int64_t s_off[kHubChunk];
+  if (static_cast<int64_t>(blockIdx.x) < a.sc.hub_ctas) {
+    const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
+    const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
+    mean_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off);
+    return;
+  }
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t slot = (static_cast<int64_t>(blockIdx.x) - a.sc.hub_ctas) * (kWarps * G) +
+                       warp * G + group;
+  const int64_t idx = a.sc.n_hub + slot;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  mean_row_regular<VEC, LPR, VPL, U>(a, r, lane_g, gmask);
+}
+
+template <int VEC, int LPR, int VPL, int U>
+int launch_mean(const MeanArgs& a, cudaStream_t s) {
+  constexpr int G = 32 / LPR;
+  const int64_t regular = a.sc.n_rows - a.sc.n_hub;
+  const int64_t grid = a.sc.hub_ctas + ceil_div(regular, kWarps * G);
+  if (grid <= 0) return GLINT_OK;
+  if (grid > 0x7fffffffLL) {
+    set_error("spmm_mean: grid too large");
+    return GLINT_EINVAL;
+  }
+  mean_kernel<VEC, LPR, VPL, U><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  return launch_status("spmm_mean");
+}
+
+int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
+  if (vec4) {
+    const int d4 = static_cast<int>(ceil_div(a.dim, 4));
+    if (d4 <= 8) return launch_mean<4, 8, 1, 8>(a, s);
+    if (d4 <= 16) return launch_mean<4, 16, 1, 8>(a, s);
+    if (d4 <= 32) return launch_mean<4, 32, 1, 8>(a, s);
+    if (d4 <= 64) return launch_mean<4, 32, 2, 4>(a, s);
+    if (d4 <= 128) return launch_mean<4, 32, 4, 2>(a, s);
+    return launch_mean<4, 32, 8, 2>(a, s);
+  }
+  if (a.dim <= 32) return launch_mean<1, 32, 1, 8>(a, s);
+  if (a.dim <= 64) return launch_mean<1, 32, 2, 8>(a, s);
+  if (a.dim <= 128) return launch_mean<1, 32, 4, 4>(a, s);
+  return launch_mean<1, 32, 8, 2>(a, s);
+}
+
+// ------------------------------------------------------- degree schedule --
+
+__global__ void sched_hist_kernel(int64_t n, RowAddr ra, unsigned long long* hist) {
+  __shared__ unsigned int sh[64];
+  if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rid = ra.csr_row(r);
+    const unsigned long long degp1 =
+        static_cast<unsigned long long>(ra.indptr[rid + 1] - ra.indptr[rid] + 1);
+    atomicAdd(&sh[63 - __clzll(degp1)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+__global__ void sched_offsets_kernel(const unsigned long long* hist, unsigned long long* offs,
+                                     int hub_log2, int64_t* n_hub_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long run = 0, hubs = 0;
+  for (int k = 63; k >= 0; --k) {
+    offs[k] = run;
+    run += hist[k];
+    if (hub_log2 >= 0 && k >= hub_log2) hubs += hist[k];
+  }
+  *n_hub_out = static_cast<int64_t>(hubs);
+}
+
+__global__ void sched_scatter_kernel(int64_t n, RowAddr ra, unsigned long long* offs,
+                                     int32_t* schedule) {
+  __shared__ unsigned int cnt[64];
+  __shared__ unsigned long long base[64];
+  for (int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x); t0 < n;
+       t0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t r = t0 + threadIdx.x;
+    int k = -1;
+    unsigned int local = 0;
+    if (r < n) {
+      const int64_t rid = ra.csr_row(r);
+      const unsigned long long degp1 =
+          static_cast<unsigned long long>(ra.indptr[rid + 1] - ra.indptr[rid] + 1);
+      k = 63 - __clzll(degp1);
+      local = atomicAdd(&cnt[k], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 64 && cnt[threadIdx.x])
+      base[threadIdx.x] = atomicAdd(&offs[threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+    __syncthreads();
+    if (k >= 0) schedule[base[k] + local] = static_cast<int32_t>(r);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- GAT --
+
+struct GatArgs {
+  RowAddr ra;
+  Sched sc;
+  int heads;
+  int head_dim;
+  int head_pitch;  // Z columns per head (multiple of 4)
+  const float* __restrict__ Z;
+  int64_t ldz;
+  const float* __restrict__ s_src;
+  const float* __restrict__ s_dst;
+  float slope;
+  float* __restrict__ out;
+  int64_t ld_out;
+};
+
+__device__ __forceinline__ float leaky(float x, float slope) {
+  return x >= 0.0f ? x : __fmul_rn(slope, x);
+}
+
+// Regular GAT row: one warp, lanes over 128-bit chunks of the head-padded Z row.
+template <int VPL, int U>
+__device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int lane,
+                                                float (*w_s)[kMaxHeads]) {
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  const int H = a.heads;
+
+  float sdst[kMaxHeads], peak[kMaxHeads], wself[kMaxHeads];
+#pragma unroll
+  for (int h = 0; h < kMaxHeads; ++h) {
+    if (h < H) {
+      sdst[h] = a.s_dst[self * H + h];
+      peak[h] = leaky(__fadd_rn(a.s_src[self * H + h], sdst[h]), a.slope);
+      wself[h] = peak[h];  // self logit, fixed up below
+    }
+  }
+  // pass 1: per-head max over edges (lanes over edges, order-free)
+  for (int64_t e = beg + lane; e < end; e += 32) {
+    const int64_t u = a.ra.map(a.ra.indices[e]);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h)
+      if (h < H) peak[h] = fmaxf(peak[h], leaky(__fadd_rn(a.s_src[u * H + h], sdst[h]), a.slope));
+  }
+#pragma unroll
+  for (int h = 0; h < kMaxHeads; ++h) {
+    if (h < H) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) peak[h] = fmaxf(peak[h], __shfl_xor_sync(0xffffffffu, peak[h], o));
+      wself[h] = expf(__fsub_rn(wself[h], peak[h]));
+    }
+  }
+
+  // lane's chunk -> head mapping
+  int head_of[VPL], j_of[VPL];
+  bool valid_chunk[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int zc = (lane + 32 * k) * 4;
+    head_of[k] = zc / a.head_pitch;
+    j_of[k] = zc - head_of[k] * a.head_pitch;
+    valid_chunk[k] = head_of[k] < H;
+    if (!valid_chunk[k]) head_of[k] = 0;
+  }
+  float num[VPL][4], den[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    den[k] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) num[k][c] = 0.0f;
+  }
+
+  for (int64_t e0 = beg; e0 < end; e0 += 32) {
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(32), end - e0));
+    int64_t my = 0;
+    if (lane < cnt) {
+      const int64_t u = a.ra.map(a.ra.indices[e0 + lane]);
+      my = u * a.ldz;
+#pragma unroll
+      for (int h = 0; h < kMaxHeads; ++h)
+        if (h < H)
+          w_s[lane][h] = expf(__fsub_rn(leaky(__fadd_rn(a.s_src[u * H + h], sdst[h]), a.slope), peak[h]));
+    }
+    __syncwarp();
+    for (int j = 0; j < cnt; j += U) {
+      float4 v[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t off = shfl64(0xffffffffu, my, (j + u) & 31, 32);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          v[u][k] = (j + u < cnt && valid_chunk[k]) ? ldg_f4(a.Z + off + (lane + 32 * k) * 4)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (j + u < cnt) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const float w = w_s[j + u][head_of[k]];
+            den[k] = __fadd_rn(den[k], w);
+            num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v[u][k].x));
+            num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v[u][k].y));
+            num[k][2] = __fadd_rn(num[k][2], __fmul_rn(w, v[u][k].z));
+            num[k][3] = __fadd_rn(num[k][3], __fmul_rn(w, v[u][k].w));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // self term last, then normalise and write the unpadded head columns
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    if (!valid_chunk[k]) continue;
+    const int hh = head_of[k];
+    const float4 zs = ldg_f4(a.Z + self * a.ldz + (lane + 32 * k) * 4);
+    const float ws = wself[hh];
+    const float d = __fadd_rn(den[k], ws);
+    const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j_of[k] + c;
+      if (j < a.head_dim) {
+        const float n = __fadd_rn(num[k][c], __fmul_rn(ws, zv[c]));
+        a.out[r * a.ld_out + hh * a.head_dim + j] = __fdiv_rn(n, d);
+      }
+    }
+  }
+}
+
+// Hub GAT row: a CTA owns (row, 256-column block of padded Z); one column per
+// thread; per chunk the CTA computes source offsets and softmax weights into
+// shared memory, then each thread walks the chunk in edge order.
+constexpr int kGatHubChunk = 256;
+
+__device__ __forceinline__ void gat_row_hub(const GatArgs& a, int64_t r, int col_block,
+                                            int64_t* s_off, float (*s_w)[kMaxHeads],
+                                            float* s_peak) {
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  const int H = a.heads;
+  using BlockReduce = cub::BlockReduce<float, kThreads>;
+  __shared__ typename BlockReduce::TempStorage tmp;
+
+  // peak per head: block-wide max over self and all edges
+  for (int h = 0; h < H; ++h) {
+    const float sd = a.s_dst[self * H + h];
+    float m = leaky(__fadd_rn(a.s_src[self * H + h], sd), a.slope);
+    for (int64_t e = beg + threadIdx.x; e < end; e += kThreads) {
+      const int64_t u = a.ra.map(a.ra.indices[e]);
+      m = fmaxf(m, leaky(__fadd_rn(a.s_src[u * H + h], sd), a.slope));
+    }
+    const float bm = BlockReduce(tmp).Reduce(m, [](float x, float y) { return fmaxf(x, y); });
+    if (threadIdx.x == 0) s_peak[h] = bm;
+    __syncthreads();
+  }
+  const int zc = col_block * kThreads + threadIdx.x;
+  const int hh = zc / a.head_pitch;
+  const int j = zc - hh * a.head_pitch;
+  const bool active = hh < H && j < a.head_dim;
+  const int hs = active ? hh : 0;
+  const float sd_h = a.s_dst[self * H + hs];
+  float num = 0.0f, den = 0.0f;
+  for (int64_t e0 = beg; e0 < end; e0 += kGatHubChunk) {
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kGatHubChunk), end - e0));
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kThreads) {
+      const int64_t u = a.ra.map(a.ra.indices[e0 + t]);
+      s_off[t] = u * a.ldz;
+      for (int h = 0; h < H; ++h) {
+        const float sd = a.s_dst[self * H + h];
+        s_w[t][h] = expf(__fsub_rn(leaky(__fadd_rn(a.s_src[u * H + h], sd), a.slope), s_peak[h]));
+      }
+    }
+    __syncthreads();
+    if (active) {
+      for (int jj = 0; jj < cnt; jj += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (jj + u < cnt) ? __ldg(a.Z + s_off[jj + u] + zc) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (jj + u < cnt) {
+            const float w = s_w[jj + u][hs];
+            den = __fadd_rn(den, w);
+            num = __fadd_rn(num, __fmul_rn(w, v[u]));
+          }
+        }
+      }
+    }
+  }
+  (void)sd_h;
+  if (active) {
+    const float ws = expf(__fsub_rn(leaky(__fadd_rn(a.s_src[self * H + hs], a.s_dst[self * H + hs]), a.slope),
+                                    s_peak[hs]));
+    const float d = __fadd_rn(den, ws);
+    const float n = __fadd_rn(num, __fmul_rn(ws, __ldg(a.Z + self * a.ldz + zc)));
+    a.out[r * a.ld_out + hh * a.head_dim + j] = __fdiv_rn(n, d);
+  }
+}
+
+template <int VPL, int U>
+__global__ void __launch_bounds__(kThreads) gat_kernel(GatArgs a) {
+  __shared__ int64_t s_off[kGatHubChunk];
+  __shared__ float s_w[kGatHubChunk][kMaxHeads];
+  __shared__ float s_peak[kMaxHeads];
+  if (static_cast<int64_t>(blockIdx.x) < a.sc.hub_ctas) {
+    const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
+    const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
+    gat_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off, s_w, s_peak);
+    return;
+  }
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t idx = a.sc.n_hub + (static_cast<int64_t>(blockIdx.x) - a.sc.hub_ctas) * kWarps + warp;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  // regular rows reuse the hub staging buffer as per-warp weight tiles
+  float(*w_s)[kMaxHeads] = s_w + warp * 32;
+  gat_row_regular<VPL, U>(a, r, lane, w_s);
+}
+
+template <int VPL, int U>
+int launch_gat(const GatArgs& a, cudaStream_t s) {
+  const int64_t grid = a.sc.hub_ctas + ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps);
+  if (grid <= 0) return GLINT_OK;
+  gat_kernel<VPL, U><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  return launch_status("gat_aggregate");
+}
+
+}  // namespace
+}  // namespace glint
+
+using namespace glint;
+
+extern "C" {
+
+int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
+                        const int32_t* indices, const int64_t* row_ids, int64_t row_base,
+                        const int64_t* self_rows, const int32_t* col_map, const float* h,
+                        int64_t ld_h, float* out, int64_t ld_out, const int32_t* schedule,
+                        int64_t n_hub, glint_stream_t stream) {
+  GLINT_REQUIRE(n_rows >= 0, "spmm_mean: n_rows must be >= 0");
+  if (n_rows == 0) return GLINT_OK;
+  GLINT_REQUIRE(dim > 0, "spmm_mean: dim must be > 0");
+  GLINT_REQUIRE(indptr && h && out, "spmm_mean: null indptr/h/out");
+  GLINT_REQUIRE(ld_h >= dim && ld_out >= dim, "spmm_mean: leading dimension < dim");
+  GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows, "spmm_mean: n_hub out of range");
+  GLINT_REQUIRE(schedule || n_hub == 0, "spmm_mean: hub rows need a schedule");
+  MeanArgs a;
+  a.ra = RowAddr{indptr, indices, row_ids, row_base, self_rows, col_map};
+  a.dim = dim;
+  a.h = h;
+  a.ld_h = ld_h;
+  a.out = out;
+  a.ld_out = ld_out;
+  a.sc.schedule = schedule;
+  a.sc.n_rows = n_rows;
+  a.sc.n_hub = n_hub;
+  a.sc.hub_col_blocks = static_cast<int>(ceil_div(dim, kThreads));
+  a.sc.hub_ctas = n_hub * a.sc.hub_col_blocks;
+  const bool vec4 = (ld_h % 4 == 0) && (ld_out % 4 == 0) && aligned16(h) && aligned16(out);
+  return dispatch_mean(a, vec4, as_stream(stream));
+}
+
+size_t glint_degree_schedule_workspace_bytes(void) { return 2 * 64 * sizeof(unsigned long long); }
+
+int glint_degree_schedule(int64_t n_rows, const int64_t* indptr, const int64_t* row_ids,
+                          int64_t row_base, int64_t hub_min_degree, int32_t* schedule_out,
+                          int64_t* n_hub_out, void* workspace, size_t workspace_bytes,
+                          glint_stream_t stream) {
+  GLINT_REQUIRE(n_rows >= 0 && n_rows < (1LL << 31), "degree_schedule: n_rows out of range");
+  GLINT_REQUIRE(indptr && schedule_out && n_hub_out && workspace, "degree_schedule: null argument");
+  GLINT_REQUIRE(workspace_bytes >= glint_degree_schedule_workspace_bytes(),
+                "degree_schedule: workspace too small");
+  GLINT_REQUIRE(hub_min_degree >= 0 && (hub_min_degree & (hub_min_degree - 1)) == 0,
+                "degree_schedule: hub_min_degree must be 0 or a power of two");
+  cudaStream_t s = as_stream(stream);
+  auto* hist = static_cast<unsigned long long*>(workspace);
+  auto* offs = hist + 64;
+  GLINT_CUDA(cudaMemsetAsync(hist, 0, 64 * sizeof(unsigned long long), s));
+  RowAddr ra{indptr, nullptr, row_ids, row_base, nullptr, nullptr};
+  int hub_log2 = -1;
+  if (hub_min_degree > 0) hub_log2 = 63 - __builtin_clzll(static_cast<unsigned long long>(hub_min_degree));
+  const int grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(n_rows, 256), 1),
+                                                      static_cast<int64_t>(sm_count()) * 8));
+  if (n_rows > 0) sched_hist_kernel<<<grid, 256, 0, s>>>(n_rows, ra, hist);
+  sched_offsets_kernel<<<1, 32, 0, s>>>(hist, offs, hub_log2, n_hub_out);
+  if (n_rows > 0) sched_scatter_kernel<<<grid, 256, 0, s>>>(n_rows, ra, offs, schedule_out);
+  return launch_status("degree_schedule");
+}
+
+int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int32_t head_pitch,
+                            const int64_t* indptr, const int32_t* indices, const int64_t* row_ids,
+                            int64_t row_base, const int64_t* self_rows, const int32_t* col_map,
+                            const float* Z, int64_t ldz, const float* s_src, const float* s_dst,
+                            float slope, float* out, int64_t ld_out, const int32_t* schedule,
+                            int64_t n_hub, glint_stream_t stream) {
+  GLINT_REQUIRE(n_rows >= 0, "gat_aggregate: n_rows must be >= 0");
+  if (n_rows == 0) return GLINT_OK;
+  GLINT_REQUIRE(heads >= 1 && heads <= kMaxHeads, "gat_aggregate: heads must be in [1, %d]", kMaxHeads);
+  GLINT_REQUIRE(head_dim >= 1 && head_pitch >= head_dim && head_pitch % 4 == 0,
+                "gat_aggregate: head_pitch must be a multiple of 4 and >= head_dim");
+  GLINT_REQUIRE(ldz % 4 == 0 && ldz >= static_cast<int64_t>(heads) * head_pitch && aligned16(Z),
+                "gat_aggregate: Z must be 16B aligned with ldz %% 4 == 0 and ldz >= heads*head_pitch");
+  GLINT_REQUIRE(indptr && Z && s_src && s_dst && out, "gat_aggregate: null argument");
+  GLINT_REQUIRE(ld_out >= static_cast<int64_t>(heads) * head_dim, "gat_aggregate: ld_out too small");
+  GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows && (schedule || n_hub == 0),
+                "gat_aggregate: bad schedule/n_hub");
+  GatArgs a;
+  a.ra = RowAddr{indptr, indices, row_ids, row_base, self_rows, col_map};
+  a.heads = heads;
+  a.head_dim = head_dim;
+  a.head_pitch = head_pitch;
+  a.Z = Z;
+  a.ldz = ldz;
+  a.s_src = s_src;
+  a.s_dst = s_dst;
+  a.slope = slope;
+  a.out = out;
+  a.ld_out = ld_out;
+  const int zw = heads * head_pitch;
+  a.sc.schedule = schedule;
+  a.sc.n_rows = n_rows;
+  a.sc.n_hub = n_hub;
+  a.sc.hub_col_blocks = static_cast<int>(ceil_div(zw, kThreads));
+  a.sc.hub_ctas = n_hub * a.sc.hub_col_blocks;
+  const int chunks = zw / 4;
+  cudaStream_t s = as_stream(stream);
+  if (chunks <= 32) return launch_gat<1, 8>(a, s);
+  if (chunks <= 64) return launch_gat<2, 4>(a, s);
+  if (chunks <= 128) return launch_gat<4, 2>(a, s);
+  GLINT_REQUIRE(chunks <= 256, "gat_aggregate: heads*head_pitch must be <= 1024");
+  return launch_gat<8, 2>(a, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Error plumbing and device queries for the C ABI.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace glint {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+void clear_error() { g_last_error.clear(); }
+
+int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: kernel launch failed: %s", what, cudaGetErrorString(e));
+    return GLINT_ECUDA;
+  }
+  return GLINT_OK;
+}
+
+int sm_count() {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+}  // namespace glint
+
+extern "C" {
+
+const char* glint_last_error(void) { return glint::g_last_error.c_str(); }
+
+int glint_abi_version(void) { return 1; }
+
+int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                      size_t* free_bytes, size_t* total_bytes) {
+  int prev = 0;
+  GLINT_CUDA(cudaGetDevice(&prev));
+  GLINT_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GLINT_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  size_t f = 0, t = 0;
+  GLINT_CUDA(cudaMemGetInfo(&f, &t));
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  GLINT_CUDA(cudaSetDevice(prev));
+  return GLINT_OK;
+}
+
+}  // extern "C"

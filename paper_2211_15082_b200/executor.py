@@ -1,0 +1,998 @@
+"""Inference engines, target annotation and the request API on B200.
+
+Drop-in for glint/executor.py: ``run_inference`` keeps the reference's
+signature, modes (full / partial / sampling), executors (layerwise /
+nodewise), orders, stats document and error behaviour
+(glint/executor.py:481-543).  What changes is where the work happens:
+
+* every stored layer output is an HBM-resident ``DeviceStore``; a block's
+  batches read neighbour rows straight from the resident input store through
+  the CSC (no per-batch gather copy of ``input_ids`` rows, which the reference
+  pays at executor.py:353-354);
+* input-domain operators (those feeding a Conv of their block) are evaluated
+  once per layer over the layer's input rows instead of once per batch
+  (results are per-row functions, so the bytes are the same);
+* a ConvMean followed by ReLU/LeakyReLU in the same block runs as
+  aggregation + one GEMM with bias and activation fused in the epilogue,
+  writing directly into the output store;
+* batch planning (the feedback controller's n_inputs count) runs on a side
+  stream with device id-set kernels, so the host sync per plan overlaps the
+  previous batch's kernels; batch membership is identical to the reference
+  for the same capacity and initial thresholds.
+
+Annotation (partial/sampling target sets) expands frontiers with the device
+id-set kernels; sampling draws (splitmix64 priorities, smallest fanout kept)
+are computed on the host as in the reference and uploaded.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, device as devmodel, kernels
+from .batching import BatchController, Thresholds
+from .errors import ConfigError, DeviceCapacityError, InternalError
+from .model_ir import ModelGraph
+from .reorder import NodeOrder, apply_order_device, make_order
+from .splitter import INPUT_REF, BlockSchedule, TensorRef, split
+from .storage import CscGraph, DeviceGraph, DeviceStore, EmbeddingStore, pitch_of
+
+MODES = ("full", "partial", "sampling")
+
+
+# ----------------------------------------------------------------- targets --
+
+
+@dataclass
+class TargetSets:
+    mode: str
+    depth: int
+    v_sets: dict
+    sampled: dict | None = None
+    skip_from: int | None = None
+
+    def graph_for_layer(self, g, layer):
+        if self.sampled is not None and layer in self.sampled:
+            return self.sampled[layer]
+        return g
+
+
+_U64 = np.uint64
+_M1 = _U64(0xBF58476D1CE4E5B9)
+_M2 = _U64(0x94D049BB133111EB)
+_GOLD = _U64(0x9E3779B97F4A7C15)
+
+
+def _mix(x):
+    """splitmix64 finaliser over uint64 arrays (wrapping arithmetic)."""
+    z = (np.asarray(x, dtype=np.uint64) + _GOLD).astype(np.uint64)
+    z = (z ^ (z >> _U64(30))) * _M1
+    z = (z ^ (z >> _U64(27))) * _M2
+    return z ^ (z >> _U64(31))
+
+
+def sample_neighbors(g, nodes, fanout, seed, layer) -> CscGraph:
+    """min(fanout, deg) distinct in-neighbours per node (glint/executor.py:74-115).
+
+    Edge priority = mix(base ^ mix(node * M1) ^ slot), base = mix(mix(seed) ^
+    mix(layer * M2)); each node keeps its `fanout` smallest priorities and the
+    kept slice is stored ascending.  Reproducible and independent of the order
+    or grouping of `nodes`.
+    """
+    if fanout < 1:
+        raise ValueError(f"fanout must be >= 1, got {fanout}")
+    indptr_h, indices_h = _host_arrays(g)
+    n = g.num_nodes
+    nodes = np.unique(np.asarray(nodes, dtype=np.int64))
+    out_ptr = np.zeros(n + 1, dtype=np.int64)
+    if len(nodes) == 0:
+        return CscGraph(n, 0, out_ptr, np.zeros(0, dtype=np.int64))
+    starts = indptr_h[nodes]
+    lens = indptr_h[nodes + 1] - starts
+    total = int(lens.sum())
+    owner = np.repeat(np.arange(len(nodes), dtype=np.int64), lens)
+    first = np.repeat(np.cumsum(lens) - lens, lens)
+    slot = np.arange(total, dtype=np.int64) - first
+    srcs = indices_h[np.repeat(starts, lens) + slot]
+    with np.errstate(over="ignore"):
+        base = _mix(_mix(np.uint64(np.int64(seed))) ^ _mix(np.uint64(layer) * _M2))
+        prio = _mix(base ^ _mix(nodes[owner].astype(np.uint64) * _M1) ^ slot.astype(np.uint64))
+    ranked = np.lexsort((prio, owner))          # by node, then priority
+    keep = ranked[slot < fanout]                 # slot == rank inside each node's run
+    k_owner, k_src = owner[keep], srcs[keep]
+    k_src = k_src[np.lexsort((k_src, k_owner))]
+    out_ptr[nodes + 1] = np.minimum(lens, fanout)
+    np.cumsum(out_ptr, out=out_ptr)
+    return CscGraph(n, int(out_ptr[-1]), out_ptr, k_src)
+
+
+def _host_arrays(g):
+    if isinstance(g, CscGraph):
+        return g.indptr, g.indices
+    key = "host_indices"
+    if key not in g._cache:
+        g._cache[key] = g.indices.cpu().numpy().astype(np.int64)
+    return g.indptr_host, g._cache[key]
+
+
+def _expand_dev(dg, nodes_np):
+    """sorted unique(nodes u in-neighbours(nodes)) via device id sets."""
+    import torch
+
+    ids = kernels.IdSet(dg.num_nodes, dg.indptr.device)
+    if len(nodes_np):
+        t = torch.from_numpy(np.ascontiguousarray(nodes_np, dtype=np.int64)).to(dg.indptr.device)
+        ids.add_ids(t).add_neighbors(dg, t)
+    ids.finalize()
+    return ids.extract().cpu().numpy()
+
+
+def skip_fires(n_next, graph) -> bool:
+    """|V[l+1]| * d_avg >= n, exact in integers (glint/executor.py:124-126)."""
+    return n_next * graph.num_edges >= graph.num_nodes * graph.num_nodes
+
+
+def annotate(g, targets, depth, mode, fanout=None, seed=0) -> TargetSets:
+    """Per-layer target sets V[depth..1] (glint/executor.py:129-164)."""
+    if mode not in MODES:
+        raise ConfigError(f"unknown inference mode {mode!r}")
+    n = g.num_nodes
+    targets = np.unique(np.asarray(targets, dtype=np.int64))
+    if len(targets) and (targets[0] < 0 or targets[-1] >= n):
+        raise ConfigError("target ids out of range")
+    sampled = None
+    if mode == "sampling":
+        if fanout is None or fanout < 1:
+            raise ConfigError("sampling mode requires fanout >= 1")
+        every = np.arange(n, dtype=np.int64)
+        sampled = {l: sample_neighbors(g, every, fanout, seed, l) for l in range(1, depth + 1)}
+    if depth == 0:
+        return TargetSets(mode, 0, {0: targets}, sampled)
+    every = np.arange(n, dtype=np.int64)
+    if mode == "full":
+        return TargetSets(mode, depth, {l: every for l in range(1, depth + 1)}, sampled)
+    v_sets = {depth: targets}
+    skip_from = None
+    for l in range(depth - 1, 0, -1):
+        g_used = sampled[l + 1] if sampled else g
+        if len(targets) and skip_fires(len(v_sets[l + 1]), g_used):
+            skip_from = l
+            for ll in range(l, 0, -1):
+                v_sets[ll] = every
+            break
+        v_sets[l] = _expand_dev(kernels.device_graph(g_used) if not isinstance(g_used, DeviceGraph)
+                                else g_used, v_sets[l + 1])
+    return TargetSets(mode, depth, v_sets, sampled, skip_from)
+
+
+# ------------------------------------------------------------------- stats --
+
+
+@dataclass
+class RunStats:
+    """Deterministic run statistics (document schema glint-stats-v1)."""
+
+    executor: str
+    mode: str
+    order: str
+    depth: int
+    initial_thresholds: tuple | None = None
+    layer_batches: dict = field(default_factory=dict)
+    layer_transfer: dict = field(default_factory=dict)
+    layer_aggregations: dict = field(default_factory=dict)
+    layer_input_bytes: dict = field(default_factory=dict)
+    total_transfer: int = 0
+    total_input_bytes: int = 0
+    total_aggregations: int = 0
+    max_footprint: int = 0
+    batches: int = 0
+    trajectory: list = field(default_factory=list)
+    batch_footprints: list = field(default_factory=list)
+    batch_transfers: list = field(default_factory=list)
+    batch_layers: list = field(default_factory=list)
+    batch_sizes: list = field(default_factory=list)
+    oom_retries: int = 0
+    thresholds_carry: bool = True
+    wall_time: float = 0.0
+
+    def _add_batch(self, layer, n_targets, fp, thresholds=None, retries=0):
+        self.batches += 1
+        for d, v in ((self.layer_batches, 1), (self.layer_transfer, fp.transfer_bytes),
+                     (self.layer_input_bytes, fp.input_bytes)):
+            d[layer] = d.get(layer, 0) + v
+        self.total_transfer += fp.transfer_bytes
+        self.total_input_bytes += fp.input_bytes
+        self.max_footprint = max(self.max_footprint, fp.peak)
+        self.oom_retries += retries
+        self.batch_footprints.append(fp.peak)
+        self.batch_transfers.append(fp.transfer_bytes)
+        self.batch_layers.append(layer)
+        self.batch_sizes.append(n_targets)
+        if thresholds is not None:
+            self.trajectory.append((layer, thresholds.n_t, thresholds.n_i))
+
+    def _add_aggregations(self, layer, count):
+        self.layer_aggregations[layer] = self.layer_aggregations.get(layer, 0) + count
+        self.total_aggregations += count
+
+    def to_lines(self) -> list:
+        kv = [("schema", "glint-stats-v1"), ("executor", self.executor), ("mode", self.mode),
+              ("order", self.order), ("depth", str(self.depth)), ("batches", str(self.batches)),
+              ("total.transfer_bytes", str(self.total_transfer)),
+              ("total.input_bytes", str(self.total_input_bytes)),
+              ("total.aggregations", str(self.total_aggregations)),
+              ("max_footprint_bytes", str(self.max_footprint)),
+              ("oom_retries", str(self.oom_retries)),
+              ("thresholds.carry_across_layers", str(self.thresholds_carry).lower())]
+        if self.initial_thresholds is not None:
+            kv.append(("thresholds.initial",
+                       f"{self.initial_thresholds[0]},{self.initial_thresholds[1]}"))
+        for l in sorted(self.layer_batches):
+            kv += [(f"layer.{l}.batches", str(self.layer_batches[l])),
+                   (f"layer.{l}.transfer_bytes", str(self.layer_transfer[l])),
+                   (f"layer.{l}.input_bytes", str(self.layer_input_bytes.get(l, 0)))]
+        for l in sorted(self.layer_aggregations):
+            kv.append((f"layer.{l}.aggregations", str(self.layer_aggregations[l])))
+        if self.trajectory:
+            kv.append(("thresholds.trajectory",
+                       ";".join(f"{l}:{a}:{b}" for l, a, b in self.trajectory)))
+        for name, vals in (("footprint_bytes", self.batch_footprints),
+                           ("transfer_bytes", self.batch_transfers),
+                           ("layer", self.batch_layers), ("targets", self.batch_sizes)):
+            if vals:
+                kv.append((f"batch.{name}", ",".join(str(v) for v in vals)))
+        return [f"{k}\t{v}" for k, v in kv]
+
+    def document(self) -> str:
+        return "\n".join(self.to_lines()) + "\n"
+
+
+def parse_stats(text) -> dict:
+    out = {}
+    for line in text.splitlines():
+        if line.strip():
+            k, _, v = line.partition("\t")
+            out[k] = v
+    return out
+
+
+# ---------------------------------------------------------- device engine --
+
+
+def _ref_key(schedule: BlockSchedule, m: ModelGraph, producer) -> str:
+    if m.operators[producer].kind == "Input":
+        return INPUT_REF
+    return TensorRef(schedule.assignment[producer], producer).key
+
+
+def _dims_table(m: ModelGraph, schedule: BlockSchedule) -> dict:
+    dims = {INPUT_REF: m.input_dim}
+    dims.update(m.out_dims)
+    for blk in schedule.blocks:
+        for ref in blk.input_refs:
+            dims[ref.key] = m.input_dim if ref.key == INPUT_REF else m.out_dims[ref.op]
+    return dims
+
+
+class _RowSpace:
+    """Rows of a device matrix: all nodes (identity) or a sorted id subset."""
+
+    def __init__(self, ids=None, rank_map=None):
+        self.ids = ids              # torch.int64 sorted, or None for identity
+        self.rank_map = rank_map    # torch.int32 [N] or None
+
+    @property
+    def identity(self):
+        return self.ids is None
+
+    def positions(self, targets):
+        """Row positions of (device int64) node ids in this space."""
+        if self.identity:
+            return targets
+        return self.rank_map.index_select(0, targets).to(targets.dtype)
+
+
+@dataclass
+class _Plan:
+    start: int
+    end: int
+    num_inputs: int
+    num_edges: int
+
+
+class _Params:
+    """Per-run device copies of model parameters (uploaded once)."""
+
+    def __init__(self, m: ModelGraph, device):
+        import torch
+
+        self.w, self.b, self.attn, self.w_pad = {}, {}, {}, {}
+        for op in m.operators.values():
+            if op.kind in ("ConvMean", "Linear"):
+                self.w[op.op_id] = torch.from_numpy(np.ascontiguousarray(
+                    op.params["weight"], dtype=np.float32)).to(device)
+                b = op.params.get("bias")
+                self.b[op.op_id] = (None if b is None else torch.from_numpy(
+                    np.ascontiguousarray(b, dtype=np.float32)).to(device))
+            elif op.kind == "ConvAttn":
+                self.w_pad[op.op_id] = kernels.padded_head_weight(
+                    torch.from_numpy(np.ascontiguousarray(op.params["weight"], np.float32)).to(device))
+                self.attn[op.op_id] = torch.from_numpy(np.ascontiguousarray(
+                    op.params["attn"], dtype=np.float32)).to(device)
+
+
+class LayerwiseEngine:
+    """Executes a BlockSchedule over HBM-resident stores (glint/executor.py:301-384)."""
+
+    def __init__(self, m: ModelGraph, schedule: BlockSchedule, g: DeviceGraph, x: DeviceStore,
+                 tsets: TargetSets, budget, thresholds: Thresholds, stats: RunStats,
+                 precision=None, row_range=None):
+        import torch
+
+        self.m, self.schedule, self.g, self.tsets = m, schedule, g, tsets
+        self.budget, self.stats = budget, stats
+        self.controller = BatchController(thresholds=thresholds, budget=budget)
+        self.dev = g.indptr.device
+        self.precision = kernels.PRECISION if precision is None else precision
+        self.params = _Params(m, self.dev)
+        self.dims = _dims_table(m, schedule)
+        self.stores = {INPUT_REF: x}
+        self.spaces = {INPUT_REF: _RowSpace()}
+        self.plan_stream = torch.cuda.Stream(device=self.dev)
+        self.users = m.consumers()
+        self.row_range = row_range          # (lo, hi) node range owned by this rank (full mode)
+        self._graph_cache = {}
+        self._plan_sets = {}
+        self._sched_cache = {}
+        self.kernel_launches = 0
+
+    # -- helpers ------------------------------------------------------------
+
+    def _graph_for(self, layer) -> DeviceGraph:
+        gl = self.tsets.graph_for_layer(self.g, layer)
+        if isinstance(gl, DeviceGraph):
+            return gl
+        dg = self._graph_cache.get(layer)
+        if dg is None:
+            dg = self._graph_cache[layer] = DeviceGraph.from_host(gl, self.dev)
+        return dg
+
+    def _hub_counter(self, gl: DeviceGraph, targets_np, full):
+        """Host prefix of hub rows (deg+1 >= HUB_MIN_DEGREE) over the layer's targets."""
+        key = ("hub", id(gl), None if full else id(targets_np))
+        pre = gl._cache.get(key)
+        if pre is None:
+            deg = gl.in_degrees if full else gl.in_degrees[targets_np]
+            pre = np.zeros(len(deg) + 1, dtype=np.int64)
+            np.cumsum(deg + 1 >= kernels.HUB_MIN_DEGREE, out=pre[1:])
+            gl._cache[key] = pre
+        return pre
+
+    def _fusions(self, blk):
+        """conv/linear op -> activation op fused into its GEMM epilogue."""
+        fused = {}
+        for o in blk.op_ids:
+            k = blk.kinds[o]
+            if k not in ("ReLU", "LeakyReLU"):
+                continue
+            x = self.m.operators[o].inputs[0]
+            if (x in blk.kinds and blk.kinds[x] in ("ConvMean", "Linear")
+                    and blk.domains[x] == "target" and blk.domains[o] == "target"
+                    and self.users[x] == [o] and x not in blk.outputs):
+                fused[x] = o
+        return fused
+
+    # -- planning -------------------------------------------------------------
+
+    def _planner(self, blk, gl, targets_dev, targets_np, full, prefix):
+        import torch
+
+        n_nodes = gl.num_nodes
+        dims = self.dims
+
+        def plan_fn(start, end):
+            n_t = end - start
+            n_e = int(prefix[end] - prefix[start]) if blk.has_conv else 0
+            if not blk.has_conv or n_t == 0:
+                n_i = n_t
+            elif full and n_t == n_nodes:
+                n_i = n_t
+            else:
+                key = id(gl)
+                ids = self._plan_sets.get(key)
+                with torch.cuda.stream(self.plan_stream):
+                    if ids is None:
+                        ids = self._plan_sets[key] = kernels.IdSet(n_nodes, self.dev)
+                    else:
+                        _lib.call("glint_idset_clear", kernels.ptr(ids.ws), ids.n,
+                                  kernels.stream_handle())
+                    if full:
+                        ids.add_ids(None, start, n_t).add_neighbors(gl, None, start, n_t)
+                    else:
+                        sl = targets_dev[start:end]
+                        ids.add_ids(sl).add_neighbors(gl, sl)
+                    ids.finalize()
+                    n_i = ids.count()
+            fp = devmodel.footprint_counts(blk, n_t, n_i, n_e, dims)
+            return _Plan(start, end, n_i, n_e), fp
+
+        return plan_fn
+
+    # -- layer-wide input-domain evaluation ---------------------------------
+
+    def _layer_inputs(self, blk, gl, targets_dev, full):
+        """Evaluate input-domain ops once over the layer's input rows R."""
+        import torch
+
+        mats, spaces = {}, {}
+        ops = [o for o in blk.op_ids if blk.domains[o] == "input"
+               and blk.kinds[o] not in ("Input", "Output")]
+        if not ops:
+            return mats, spaces
+        if full:
+            space = _RowSpace()
+            n_rows = gl.num_nodes
+        else:
+            ids = kernels.IdSet(gl.num_nodes, self.dev)
+            ids.add_ids(targets_dev).add_neighbors(gl, targets_dev).finalize()
+            rows = ids.extract()
+            space = _RowSpace(rows, ids.rank_map())
+            n_rows = int(rows.shape[0])
+        for o in ops:
+            op = self.m.operators[o]
+            operands, row_sel = [], []
+            for p in op.inputs:
+                if p in mats:
+                    operands.append(mats[p])
+                    row_sel.append(None)
+                else:
+                    st = self.stores[_ref_key(self.schedule, self.m, p)]
+                    sp = self.spaces[_ref_key(self.schedule, self.m, p)]
+                    operands.append(st.view())
+                    if space.identity and sp.identity:
+                        row_sel.append(None)
+                    else:
+                        sel = space.ids if not space.identity else torch.arange(
+                            n_rows, device=self.dev, dtype=torch.int64)
+                        row_sel.append(sp.positions(sel))
+            width = self.m.out_dims[o]
+            out = torch.empty((n_rows, pitch_of(width)), dtype=torch.float32, device=self.dev)[:, :width]
+            self._eval_normal_into(out, op, operands, row_sel, fused_act=None)
+            mats[o] = out
+            spaces[o] = space
+        return mats, spaces
+
+    # -- operator evaluation --------------------------------------------------
+
+    def _eval_normal_into(self, out, op, operands, row_sel, fused_act=None):
+        k = op.kind
+        if k == "Linear":
+            act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
+                   "LeakyReLU": _lib.ACT_LEAKY_RELU}[fused_act]
+            kernels.linear_into(out, operands[0], self.params.w[op.op_id], self.params.b[op.op_id],
+                                act, a_rows=row_sel[0], precision=self.precision)
+        elif k == "Concat":
+            col = 0
+            for mat, rs in zip(operands, row_sel):
+                w = int(mat.shape[1])
+                kernels.copy_rows(out[:, col:col + w], mat, src_rows=rs, n_rows=out.shape[0])
+                col += w
+        elif k in kernels.ELEMENTWISE_KINDS:
+            n = len(operands)
+            if n <= 8:
+                kernels.elementwise_into(out, k, operands, row_sel)
+            else:
+                kernels.elementwise_into(out, k, operands[:8], row_sel[:8])
+                rest, rrest = operands[8:], row_sel[8:]
+                while rest:
+                    kernels.elementwise_into(out, k, [out] + rest[:7], [None] + rrest[:7])
+                    rest, rrest = rest[7:], rrest[7:]
+        else:
+            raise InternalError(f"unexpected operator kind {k}")
+        self.kernel_launches += 1
+
+    # -- one block ------------------------------------------------------------
+
+    def run_block(self, blk):
+        import torch
+
+        m = self.m
+        layer = blk.layer
+        targets_np = self.tsets.v_sets[layer]
+        gl = self._graph_for(layer) if blk.has_conv else self.g
+        n_nodes = self.g.num_nodes
+        full = len(targets_np) == n_nodes
+        lo, hi = 0, len(targets_np)
+        if self.row_range is not None and full:
+            lo, hi = self.row_range
+        targets_dev = None if full else torch.from_numpy(
+            np.ascontiguousarray(targets_np, dtype=np.int64)).to(self.dev)
+
+        # output stores
+        if full:
+            out_space = _RowSpace()
+        else:
+            ids = kernels.IdSet(n_nodes, self.dev)
+            ids.add_ids(targets_dev).finalize()
+            out_space = _RowSpace(targets_dev, ids.rank_map())
+        for o in blk.outputs:
+            key = TensorRef(blk.block_id, o).key
+            self.stores[key] = DeviceStore(len(targets_np), m.out_dims[o], self.dev,
+                                           rows=out_space.ids, rank_map=out_space.rank_map)
+            self.spaces[key] = out_space
+
+        if blk.has_conv:
+            prefix = (gl.indptr_host if full else
+                      _prefix_host(gl.in_degrees, targets_np))
+        else:
+            prefix = np.zeros(len(targets_np) + 1, dtype=np.int64)
+        hub_pre = self._hub_counter(gl, targets_np, full) if blk.has_conv else None
+        layer_mats, layer_spaces = self._layer_inputs(blk, gl, targets_dev, full)
+        fused = self._fusions(blk)
+        gat_cache = {}
+        n_convs = sum(1 for _, k, _ in blk.iter_ops() if k in ("ConvMean", "ConvAttn"))
+
+        def execute(plan: _Plan):
+            self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
+                            hub_pre, gat_cache)
+
+        self.plan_stream.wait_stream(torch.cuda.current_stream(self.dev))
+        plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix)
+        sub_targets = targets_np[lo:hi] if (lo, hi) != (0, len(targets_np)) else targets_np
+        sub_prefix = prefix[lo:hi + 1] - prefix[lo] if (lo, hi) != (0, len(targets_np)) else prefix
+
+        def plan_off(start, end):
+            plan, fp = plan_fn(start + lo, end + lo)
+            return plan, fp
+
+        records = self.controller.run_layer(layer, sub_targets, sub_prefix, plan_off, execute)
+        for rec in records:
+            self.stats._add_batch(layer, rec.n_targets, rec.footprint,
+                                  Thresholds(rec.n_t, rec.n_i), rec.oom_retries)
+            self.stats._add_aggregations(layer, n_convs * rec.n_targets)
+        return records
+
+    def _run_batch(self, blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
+                   hub_pre, gat_cache):
+        import torch
+
+        m = self.m
+        s, e = plan.start, plan.end
+        B = e - s
+        if B == 0:
+            return
+        row_ids = None if full else targets_dev[s:e]
+        row_base = s if full else 0
+        batch_nodes = (torch.arange(s, e, device=self.dev, dtype=torch.int64) if full
+                       else row_ids)
+        mats = {}
+        out_keys = {o: TensorRef(blk.block_id, o).key for o in blk.outputs}
+
+        def dest(o, width):
+            """Output buffer for op o: the store slice when o is a stored output."""
+            if o in out_keys and blk.domains[o] == "target":
+                return self.stores[out_keys[o]].data[s:e, :width]
+            return torch.empty((B, pitch_of(width)), dtype=torch.float32, device=self.dev)[:, :width]
+
+        def operand(p):
+            """(matrix, row selector) of operand p restricted to the batch targets."""
+            if p in mats:
+                return mats[p], None
+            if p in layer_mats:
+                sp = layer_spaces[p]
+                if sp.identity:
+                    return layer_mats[p][s:e] if full else layer_mats[p], (None if full else row_ids)
+                return layer_mats[p], sp.positions(batch_nodes)
+            key = _ref_key(self.schedule, m, p)
+            st, sp = self.stores[key], self.spaces[key]
+            if sp.identity:
+                return (st.view()[s:e], None) if full else (st.view(), row_ids)
+            return st.view(), sp.positions(batch_nodes)
+
+        def conv_source(p):
+            """(matrix over some row space, col_map) feeding a conv."""
+            if p in layer_mats:
+                sp = layer_spaces[p]
+                return layer_mats[p], sp.rank_map
+            key = _ref_key(self.schedule, m, p)
+            return self.stores[key].view(), self.spaces[key].rank_map
+
+        sched = self._schedule(gl, row_ids, row_base, B, full) if blk.has_conv else None
+        n_hub = int(hub_pre[e] - hub_pre[s]) if hub_pre is not None else 0
+
+        skip = set(fused.values())
+        for o in blk.op_ids:
+            op = m.operators[o]
+            if op.kind in ("Input", "Output") or blk.domains[o] == "input" or o in skip:
+                continue
+            if op.kind == "ConvMean":
+                h, cmap = conv_source(op.inputs[0])
+                d_in = int(h.shape[1])
+                agg = torch.empty((B, pitch_of(d_in)), dtype=torch.float32, device=self.dev)[:, :d_in]
+                kernels.spmm_mean(agg, h, gl.indptr, gl.indices, B, row_ids=row_ids,
+                                  row_base=row_base, col_map=cmap, schedule=sched, n_hub=n_hub)
+                act_op = fused.get(o)
+                target = act_op or o
+                out = dest(target, m.out_dims[o])
+                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
+                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                kernels.linear_into(out, agg, self.params.w[o], self.params.b[o], act,
+                                    precision=self.precision)
+                self.kernel_launches += 2
+                mats[target] = out
+                if act_op is None:
+                    mats[o] = out
+            elif op.kind == "ConvAttn":
+                h, cmap = conv_source(op.inputs[0])
+                W = op.params["weight"]
+                H, dh = int(W.shape[0]), int(W.shape[1])
+                if o not in gat_cache:
+                    gat_cache[o] = kernels.attn_project(h, self.params.w_pad[o], self.params.attn[o],
+                                                        H, dh, precision=self.precision)
+                    self.kernel_launches += 2
+                Z, s_src, s_dst = gat_cache[o]
+                out = dest(o, H * dh)
+                kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, gl.indptr, gl.indices, B,
+                                      row_ids=row_ids, row_base=row_base, col_map=cmap,
+                                      schedule=sched, n_hub=n_hub)
+                self.kernel_launches += 1
+                mats[o] = out
+            else:
+                ops_, sels = zip(*(operand(p) for p in op.inputs))
+                act_op = fused.get(o)
+                target = act_op or o
+                out = dest(target, m.out_dims[o])
+                self._eval_normal_into(out, op, list(ops_), list(sels),
+                                       fused_act=m.operators[act_op].kind if act_op else None)
+                mats[target] = out
+                if act_op is None:
+                    mats[o] = out
+
+        for o in blk.outputs:
+            st = self.stores[out_keys[o]]
+            if blk.domains[o] == "input":
+                src, sel = operand(o)
+                kernels.copy_rows(st.data[s:e, :st.dim], src, src_rows=sel, n_rows=B)
+                self.kernel_launches += 1
+            else:
+                mat = mats[o]
+                view = st.data[s:e, :st.dim]
+                if mat.data_ptr() != view.data_ptr():
+                    kernels.copy_rows(view, mat)
+                    self.kernel_launches += 1
+
+    def _schedule(self, gl, row_ids, row_base, B, full):
+        if not full:
+            sched, _ = kernels.degree_schedule(gl.indptr, row_ids, 0, B)
+            self.kernel_launches += 3
+            return sched
+        key = (id(gl), row_base, B)
+        sched = self._sched_cache.get(key)
+        if sched is None:
+            sched, _ = kernels.degree_schedule(gl.indptr, None, row_base, B)
+            self._sched_cache = {key: sched}
+            self.kernel_launches += 3
+        return sched
+
+    def release_after(self, blk):
+        out_key = self.schedule.model_output.key
+        for key, last in self.schedule.drop_after.items():
+            if last == blk.block_id and key not in (INPUT_REF, out_key):
+                st = self.stores.pop(key, None)
+                if st is not None:
+                    st.release()
+
+    def run(self, exchange=None):
+        for blk in self.schedule.blocks:
+            self.run_block(blk)
+            if exchange is not None:
+                exchange(self, blk)
+            self.release_after(blk)
+        return self.stores[self.schedule.model_output.key]
+
+
+def _prefix_host(degs, targets_np):
+    pre = np.zeros(len(targets_np) + 1, dtype=np.int64)
+    if len(targets_np):
+        np.cumsum(degs[targets_np], out=pre[1:])
+    return pre
+
+
+def infer_layerwise(m: ModelGraph, schedule: BlockSchedule, g, x_store, tsets: TargetSets,
+                    budget, thresholds: Thresholds, stats: RunStats, store_backing="memory",
+                    workdir=None, precision=None):
+    """Execute the block schedule; returns the model-output DeviceStore."""
+    dg = kernels.device_graph(g)
+    x = _as_device_store(x_store, dg.device)
+    eng = LayerwiseEngine(m, schedule, dg, x, tsets, budget, thresholds, stats, precision)
+    return eng.run()
+
+
+# --------------------------------------------------------------- nodewise --
+
+
+def infer_nodewise(m: ModelGraph, g, x_store, targets, batch_size, budget, stats: RunStats,
+                   sampled=None, precision=None):
+    """Per-chunk multi-hop evaluation of the unsplit DAG (glint/executor.py:387-469).
+
+    The correctness baseline: recomputes shared neighbours per chunk.  Runs on
+    the device with the same kernels; a footprint over capacity is a hard
+    DeviceCapacityError.
+    """
+    import torch
+
+    if batch_size < 1:
+        raise ConfigError(f"batch size must be >= 1, got {batch_size}")
+    dg = kernels.device_graph(g)
+    x = _as_device_store(x_store, dg.device).view()
+    targets = np.asarray(targets, dtype=np.int64)
+    out = torch.zeros((len(targets), m.output_dim), dtype=torch.float32, device=dg.device)
+    graphs = {}
+
+    def graph_for(layer):
+        if sampled is not None and layer in sampled:
+            if layer not in graphs:
+                graphs[layer] = DeviceGraph.from_host(sampled[layer], dg.device)
+            return graphs[layer]
+        return dg
+
+    params = _Params(m, dg.device)
+    for start in range(0, len(targets), batch_size):
+        chunk = targets[start:start + batch_size]
+        chunk_sorted = np.unique(chunk)
+        need = {m.output_id: chunk_sorted}
+        for op_id in reversed(m.topo_order):
+            cur = need.get(op_id)
+            op = m.operators[op_id]
+            if cur is None or op.kind == "Input":
+                continue
+            req = _expand_dev(graph_for(m.layer_of[op_id]), cur) if op.is_conv else cur
+            for p in op.inputs:
+                need[p] = np.union1d(need[p], req) if p in need else req
+        slice_b = inter_b = 0
+        agg_counts, bcs = {}, {}
+        for op_id in m.topo_order:
+            op = m.operators[op_id]
+            if op_id not in need or op.kind in ("Input", "Output"):
+                continue
+            inter_b += len(need[op_id]) * m.out_dims[op_id] * devmodel.VALUE_BYTES
+            if op.is_conv:
+                bc = kernels.build_batch_csc(graph_for(m.layer_of[op_id]), need[op_id])
+                bcs[op_id] = bc
+                slice_b += (bc.num_targets + 1 + bc.num_edges) * devmodel.ID_BYTES
+                lay = m.layer_of[op_id]
+                agg_counts[lay] = agg_counts.get(lay, 0) + bc.num_targets
+        in_b = len(need[m.input_id]) * m.input_dim * devmodel.VALUE_BYTES
+        out_b = len(chunk) * m.output_dim * devmodel.VALUE_BYTES
+        fp = devmodel.BatchFootprint(slice_b, in_b, inter_b, out_b)
+        if fp.peak > budget.capacity:
+            raise DeviceCapacityError(
+                f"node-wise batch of {len(chunk)} targets needs {fp.peak} B, "
+                f"over device capacity {budget.capacity} B")
+        need_dev = {k: torch.from_numpy(v).to(dg.device) for k, v in need.items()}
+        mats = {m.input_id: x.index_select(0, need_dev[m.input_id])}
+
+        def rows_of(p, ids_dev):
+            return torch.searchsorted(need_dev[p], ids_dev)
+
+        for op_id in m.topo_order:
+            op = m.operators[op_id]
+            if op_id not in need or op.kind in ("Input", "Output"):
+                continue
+            if op.is_conv:
+                bc = bcs[op_id]
+                p = op.inputs[0]
+                h = mats[p].index_select(0, rows_of(p, bc.input_ids))
+                mats[op_id] = _eval_conv_dev(op, bc, h, params, precision)
+            else:
+                rows = need_dev[op_id]
+                mats[op_id] = _eval_normal_dev(
+                    op, [mats[p].index_select(0, rows_of(p, rows)) for p in op.inputs], params,
+                    precision)
+        prod = m.operators[m.output_id].inputs[0]
+        ck = torch.from_numpy(chunk).to(dg.device)
+        out[start:start + len(chunk)] = mats[prod].index_select(0, rows_of(prod, ck))
+        stats._add_batch(0, len(chunk), fp)
+        for lay, cnt in sorted(agg_counts.items()):
+            stats._add_aggregations(lay, cnt)
+    return out
+
+
+def _eval_conv_dev(op, bc, h, params, precision):
+    import torch
+
+    if op.kind == "ConvMean":
+        agg = kernels.agg_mean(bc, h)
+        out = torch.empty((agg.shape[0], params.w[op.op_id].shape[0]), dtype=torch.float32,
+                          device=h.device)
+        return kernels.linear_into(out, agg, params.w[op.op_id], params.b[op.op_id],
+                                   _lib.ACT_NONE, precision=precision)
+    W = op.params["weight"]
+    H, dh = int(W.shape[0]), int(W.shape[1])
+    Z, s_src, s_dst = kernels.attn_project(h, params.w_pad[op.op_id], params.attn[op.op_id], H,
+                                           dh, precision=precision)
+    out = torch.empty((bc.num_targets, H * dh), dtype=torch.float32, device=h.device)
+    if bc.num_targets:
+        sched, n_hub = kernels._local_schedule(bc.indptr, bc.num_targets)
+        kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, bc.indptr, bc.local32, bc.num_targets,
+                              self_rows=bc.target_pos, schedule=sched, n_hub=n_hub)
+    return out
+
+
+def _eval_normal_dev(op, mats, params, precision):
+    import torch
+
+    if op.kind == "Linear":
+        w = params.w[op.op_id]
+        out = torch.empty((mats[0].shape[0], w.shape[0]), dtype=torch.float32,
+                          device=mats[0].device)
+        return kernels.linear_into(out, mats[0], w, params.b[op.op_id], _lib.ACT_NONE,
+                                   precision=precision)
+    if op.kind == "Concat":
+        return kernels.concat(mats)
+    return kernels.elementwise(op.kind, mats)
+
+
+# ------------------------------------------------------------- request API --
+
+
+@dataclass
+class InferenceResult:
+    output: object                # numpy (host inputs) or CUDA tensor; user target order
+    target_ids: np.ndarray
+    stats: RunStats
+    order: NodeOrder
+    schedule: BlockSchedule | None = None
+    budget: object = None
+
+
+def _as_device_store(x, device) -> DeviceStore:
+    import torch
+
+    if isinstance(x, DeviceStore):
+        return x
+    arr = x.to_array() if isinstance(x, EmbeddingStore) else x
+    t = kernels.to_device(arr, torch.float32, device)
+    n, d = int(t.shape[0]), int(t.shape[1])
+    if d % 4 == 0 and t.is_contiguous():
+        return DeviceStore(n, d, t.device, data=t)
+    st = DeviceStore(n, d, t.device)
+    kernels.copy_rows(st.view(), t)
+    return st
+
+
+def _dims_of(x):
+    if isinstance(x, (EmbeddingStore, DeviceStore)):
+        return x.num_rows, x.dim
+    return int(x.shape[0]), int(x.shape[1])
+
+
+def resolve_budget(budget, resident_bytes=0):
+    if budget is None:
+        raise ConfigError("a device budget is required")
+    if isinstance(budget, str):
+        if budget != "device":
+            raise ConfigError(f"unknown budget spec {budget!r}")
+        return devmodel.DeviceBudget.from_device(reserve_bytes=resident_bytes)
+    return budget
+
+
+def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanout=None, seed=0,
+                  executor="layerwise", order="none", budget=None, thresholds=None,
+                  batch_size=1024, store_backing="memory", workdir=None, output="auto",
+                  precision=None) -> InferenceResult:
+    """End to end: reorder, annotate, execute, de-permute (glint/executor.py:481-543).
+
+    ``budget`` may be a DeviceBudget (reference behaviour) or ``"device"``:
+    capacity from free HBM after the resident stores are planned.
+    ``output``: "numpy", "device" or "auto" (numpy when the features came
+    from the host).  ``store_backing="file"`` is accepted for compatibility;
+    stores stay HBM-resident either way (outputs are identical).
+    """
+    import torch
+
+    if mode == "partial" and targets is None:
+        raise ConfigError("partial mode requires a target list")
+    if mode == "sampling" and (fanout is None or fanout < 1):
+        raise ConfigError("sampling mode requires fanout >= 1")
+    if budget is None:
+        raise ConfigError("a device budget is required")
+    n_rows, dim = _dims_of(x_store)
+    if n_rows != g.num_nodes or dim != m.input_dim:
+        raise ConfigError(f"features ({n_rows}x{dim}) do not match "
+                          f"graph ({g.num_nodes} nodes) and model input dim {m.input_dim}")
+    if mode not in MODES:
+        raise ConfigError(f"unknown inference mode {mode!r}")
+    if executor not in ("layerwise", "nodewise"):
+        raise ConfigError(f"unknown executor {executor!r}")
+    if mode == "full" or targets is None:
+        user_targets = np.arange(g.num_nodes, dtype=np.int64)
+    else:
+        user_targets = np.asarray(targets, dtype=np.int64)
+        if len(user_targets) != len(np.unique(user_targets)):
+            raise ConfigError("duplicate target ids")
+        if len(user_targets) and (user_targets.min() < 0 or user_targets.max() >= g.num_nodes):
+            raise ConfigError("target ids out of range")
+    host_out = (output == "numpy") or (output == "auto" and not isinstance(
+        x_store, (torch.Tensor, DeviceStore)))
+
+    node_order = make_order(g, order, seed)
+    dg0 = kernels.device_graph(g)
+    x0 = _as_device_store(x_store, dg0.device)
+    g_i, x_i = apply_order_device(dg0, x0, node_order)
+    internal = np.sort(node_order.inv[user_targets]) if len(user_targets) else user_targets
+    thresholds = thresholds or Thresholds(n_t=1024, n_i=32768)
+    stats = RunStats(executor=executor, mode=mode, order=order, depth=m.depth,
+                     initial_thresholds=(thresholds.n_t, thresholds.n_i)
+                     if executor == "layerwise" else None)
+    started = time.perf_counter()
+    tsets = annotate(g_i if mode != "sampling" else g_i.to_host(), internal, m.depth, mode,
+                     fanout, seed)
+    schedule = None
+    if executor == "layerwise":
+        schedule = split(m)
+        bud = resolve_budget(budget, _resident_bytes(m, schedule, tsets, g_i))
+        eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision)
+        store = eng.run()
+        row_ids = tsets.v_sets[m.depth if m.depth else 0]
+        out_dev = _gather_rows(store, row_ids, node_order.inv[user_targets], dg0.device)
+    else:
+        bud = resolve_budget(budget)
+        out_sorted = infer_nodewise(m, g_i, x_i, internal, batch_size, bud, stats,
+                                    sampled=tsets.sampled, precision=precision)
+        row_ids = internal
+        out_dev = _gather_dense(out_sorted, row_ids, node_order.inv[user_targets])
+    torch.cuda.synchronize(dg0.device)
+    stats.wall_time = time.perf_counter() - started
+    output_val = out_dev.cpu().numpy() if host_out else out_dev
+    return InferenceResult(output=output_val, target_ids=user_targets, stats=stats,
+                           order=node_order, schedule=schedule, budget=bud)
+
+
+def _resident_bytes(m, schedule, tsets, g):
+    """Upper bound of resident store bytes alive at once (for budget='device')."""
+    live = 0
+    peak = 0
+    sizes = {}
+    for blk in schedule.blocks:
+        rows = len(tsets.v_sets[blk.layer])
+        for o in blk.outputs:
+            sizes[TensorRef(blk.block_id, o).key] = rows * pitch_of(m.out_dims[o]) * 4
+            live += sizes[TensorRef(blk.block_id, o).key]
+        peak = max(peak, live)
+        for key, last in schedule.drop_after.items():
+            if last == blk.block_id and key in sizes:
+                live -= sizes.pop(key)
+    return peak
+
+
+def _gather_rows(store: DeviceStore, row_ids, wanted, device):
+    """Rows of `store` (rows = sorted row_ids) for internal ids `wanted`, in order."""
+    import torch
+
+    pos = np.searchsorted(row_ids, wanted)
+    if len(wanted):
+        safe = np.minimum(pos, len(row_ids) - 1)
+        if not np.array_equal(row_ids[safe], wanted):
+            raise InternalError("output rows do not cover the requested targets")
+    out = torch.empty((len(wanted), store.dim), dtype=torch.float32, device=device)
+    if len(wanted):
+        kernels.copy_rows(out, store.view(), src_rows=torch.from_numpy(pos.astype(np.int64)).to(device))
+    return out
+
+
+def _gather_dense(mat, row_ids, wanted):
+    import torch
+
+    pos = np.searchsorted(row_ids, wanted)
+    if len(wanted):
+        safe = np.minimum(pos, len(row_ids) - 1)
+        if not np.array_equal(row_ids[safe], wanted):
+            raise InternalError("output rows do not cover the requested targets")
+    out = torch.empty((len(wanted), mat.shape[1]), dtype=torch.float32, device=mat.device)
+    if len(wanted):
+        kernels.copy_rows(out, mat, src_rows=torch.from_numpy(pos.astype(np.int64)).to(mat.device))
+    return out

@@ -1,0 +1,151 @@
+"""End-to-end parity of run_inference on the GPU against the reference's own runs.
+
+For every golden case (graphs x models x modes x orders x budgets, produced by
+running the reference): the stats document -- batch membership, OOM retries,
+threshold trajectory, footprints, transfer/input bytes, aggregation counts --
+must be byte-identical, and the output embeddings within rel-L2 <= 1e-4.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_graph, rel_l2
+from oracle import glint_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, arrs, models, **over):
+    from paper_2211_15082_b200.batching import Thresholds
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+
+    g = golden_graph(arrs, case["graph"])
+    x = arrs[f"e/{case['graph']}/x"]
+    kw = dict(mode=case["mode"], order=case["order"], seed=case.get("seed", 13),
+              budget=DeviceBudget(case["budget"]),
+              thresholds=Thresholds(*case.get("thresholds", [64, 512])))
+    if case["mode"] != "full":
+        kw["targets"] = (arrs[f"e/{case['graph']}/partial"] if case["graph"] != "toy"
+                         else np.array([3, 0]))
+    if case["mode"] == "sampling":
+        kw["fanout"] = case["fanout"]
+    kw.update(over)
+    return run_inference(models[case["model"]], g, x, **kw)
+
+
+def test_all_golden_cases(golden, cuda):
+    from test_host_logic import golden_models
+
+    arrs, meta = golden
+    models = golden_models()
+    worst = 0.0
+    for case in meta["e2e"]:
+        res = _run(case, arrs, models)
+        assert res.stats.document() == case["stats"], case["name"]
+        err = rel_l2(res.output, arrs[case["output"]])
+        worst = max(worst, err)
+        assert err <= 1e-4, (case["name"], err)
+    print(f"worst rel-L2 over {len(meta['e2e'])} cases: {worst:.2e}")
+
+
+def test_nodewise_equals_layerwise_bytes(golden, cuda):
+    """Both engines share kernels; batch invariance makes them bit-identical
+    (reference test_executor.py:109-180)."""
+    from test_host_logic import golden_models
+
+    arrs, meta = golden
+    models = golden_models()
+    done = 0
+    for case in meta["e2e"]:
+        if case["graph"] not in ("toy", "reg200") or case["budget"] != 1 << 30:
+            continue
+        lw = _run(case, arrs, models)
+        nw = _run(case, arrs, models, executor="nodewise", batch_size=7)
+        assert lw.output.tobytes() == nw.output.tobytes(), case["name"]
+        done += 1
+    assert done >= 8
+
+
+def test_outputs_invariant_to_batching_and_order(golden, cuda):
+    from paper_2211_15082_b200.batching import Thresholds
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn, build_jknet
+
+    arrs, _ = golden
+    g = golden_graph(arrs, "pow300")
+    x = arrs["e/pow300/x"]
+    for m in (build_gcn(8, 16, 4, 3, seed=1), build_jknet(8, 6, 4, 3, seed=2)):
+        base = run_inference(m, g, x, budget=DeviceBudget(1 << 30)).output
+        for th in (Thresholds(1, 10 ** 6), Thresholds(7, 40), Thresholds(1000, 10 ** 6)):
+            for order in ("none", "rcmk", "degree", "random"):
+                out = run_inference(m, g, x, budget=DeviceBudget(1 << 30), thresholds=th,
+                                    order=order, seed=3).output
+                assert out.tobytes() == base.tobytes(), (th, order)
+
+
+def test_device_budget_and_device_output(golden, cuda):
+    import torch
+
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn
+
+    arrs, _ = golden
+    g = golden_graph(arrs, "reg200")
+    x = arrs["e/reg200/x"]
+    m = build_gcn(8, 16, 4, 2, seed=5)
+    res = run_inference(m, g, torch.from_numpy(x).cuda(), budget="device")
+    assert isinstance(res.output, torch.Tensor) and res.output.is_cuda
+    want = orc.eval_model(orc.model_spec(m), g.indptr, g.indices, x)
+    assert rel_l2(res.output.cpu().numpy(), want) <= 1e-5
+    assert res.budget.capacity > 1 << 30
+
+
+def test_partial_outputs_in_listed_order(golden, cuda):
+    """Reference test_executor.py:120-128."""
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn, gen_features
+
+    arrs, _ = golden
+    toy = golden_graph(arrs, "toy")
+    m = build_gcn(3, 4, 2, layers=2, seed=2)
+    x = gen_features(6, 3, seed=0)
+    big = DeviceBudget(1 << 30)
+    full = run_inference(m, toy, x, budget=big)
+    part = run_inference(m, toy, x, mode="partial", targets=[3, 0], budget=big)
+    assert part.output.shape == (2, 2)
+    assert part.output[0].tobytes() == full.output[3].tobytes()
+    assert part.output[1].tobytes() == full.output[0].tobytes()
+
+
+def test_repetition_elimination_counts(golden, cuda):
+    """Reference test_executor.py:183-196: node-wise 6 vs layer-wise 4 aggregations."""
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn, gen_features
+
+    arrs, _ = golden
+    toy = golden_graph(arrs, "toy")
+    m = build_gcn(1, 2, 2, layers=2, seed=0)
+    x = gen_features(6, 1, seed=0)
+    big = DeviceBudget(1 << 30)
+    nw = run_inference(m, toy, x, mode="partial", targets=[0, 1], executor="nodewise",
+                       budget=big, batch_size=1)
+    lw = run_inference(m, toy, x, mode="partial", targets=[0, 1], budget=big)
+    assert nw.stats.layer_aggregations[1] == 6
+    assert lw.stats.layer_aggregations[1] == 4
+
+
+def test_nodewise_hard_oom(golden, cuda):
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.errors import DeviceCapacityError
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn, gen_features
+
+    arrs, _ = golden
+    toy = golden_graph(arrs, "toy")
+    with pytest.raises(DeviceCapacityError):
+        run_inference(build_gcn(3, 4, 2, 2, seed=2), toy, gen_features(6, 3, 0),
+                      executor="nodewise", budget=DeviceBudget(64), batch_size=6)
