@@ -96,8 +96,17 @@ def last_error() -> str:
     return msg.decode(errors="replace") if msg else ""
 
 
+# Kernels launched per call (for the bench's launch count); host-only or
+# memset-only entry points launch none.
+KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
+                    "glint_degree_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
+                    "glint_device_info": 0}
+LAUNCHES = [0]
+
+
 def call(name, *args):
     """Invoke an int-returning entry point and map its status to an exception."""
+    LAUNCHES[0] += KERNELS_PER_CALL.get(name, 1)
     rc = getattr(load(), name)(*args)
     if rc == GLINT_OK:
         return

@@ -40,7 +40,7 @@ __global__ void scan_reduce_kernel(int64_t n, F f, int64_t* partials) {
   if (threadIdx.x == 0) partials[blockIdx.x] = t;
 }
 
-__global__ void scan_partials_kernel(int64_t nt, int64_t* partials) {
+__global__ void __launch_bounds__(1024) scan_partials_kernel(int64_t nt, int64_t* partials) {
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   int64_t carry = 0;

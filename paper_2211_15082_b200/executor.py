@@ -348,6 +348,7 @@ class LayerwiseEngine:
         self._plan_sets = {}
         self._sched_cache = {}
         self.kernel_launches = 0
+        self.probe = None               # optional KernelProbe (bench roofline timing)
 
     # -- helpers ------------------------------------------------------------
 
@@ -612,15 +613,23 @@ class LayerwiseEngine:
                 h, cmap = conv_source(op.inputs[0])
                 d_in = int(h.shape[1])
                 agg = torch.empty((B, pitch_of(d_in)), dtype=torch.float32, device=self.dev)[:, :d_in]
+                if self.probe is not None:
+                    self.probe.begin("spmm_mean")
                 kernels.spmm_mean(agg, h, gl.indptr, gl.indices, B, row_ids=row_ids,
                                   row_base=row_base, col_map=cmap, schedule=sched, n_hub=n_hub)
+                if self.probe is not None:
+                    self.probe.end(agg_bytes(d_in, plan.num_edges, B))
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, m.out_dims[o])
                 act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
                        "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                if self.probe is not None:
+                    self.probe.begin("linear")
                 kernels.linear_into(out, agg, self.params.w[o], self.params.b[o], act,
                                     precision=self.precision)
+                if self.probe is not None:
+                    self.probe.end(2 * B * d_in * m.out_dims[o])   # FLOPs
                 self.kernel_launches += 2
                 mats[target] = out
                 if act_op is None:
@@ -635,9 +644,13 @@ class LayerwiseEngine:
                     self.kernel_launches += 2
                 Z, s_src, s_dst = gat_cache[o]
                 out = dest(o, H * dh)
+                if self.probe is not None:
+                    self.probe.begin("gat_aggregate")
                 kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, gl.indptr, gl.indices, B,
                                       row_ids=row_ids, row_base=row_base, col_map=cmap,
                                       schedule=sched, n_hub=n_hub)
+                if self.probe is not None:
+                    self.probe.end(agg_bytes(H * dh, plan.num_edges, B, heads=H))
                 self.kernel_launches += 1
                 mats[o] = out
             else:
@@ -692,6 +705,48 @@ class LayerwiseEngine:
                 exchange(self, blk)
             self.release_after(blk)
         return self.stores[self.schedule.model_output.key]
+
+
+def agg_bytes(width, n_edges, n_rows, heads=0) -> int:
+    """Algorithmic HBM bytes of one aggregation launch (SURVEY §8d B_agg):
+    gathered fp32 source rows + self rows, int32 indices, int64 indptr, and for
+    attention the per-head scores (s_src per edge and self, s_dst per target)."""
+    b = 4 * width * (n_edges + n_rows) + 4 * n_edges + 8 * (n_rows + 1)
+    if heads:
+        b += 4 * heads * (n_edges + 2 * n_rows)
+    return b
+
+
+class KernelProbe:
+    """CUDA-event timing of selected launches on the launching stream."""
+
+    def __init__(self):
+        self.records = []
+        self._open = None
+
+    def begin(self, name):
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self._open = (name, ev)
+
+    def end(self, nbytes):
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        name, start = self._open
+        self.records.append((name, nbytes, start, ev))
+        self._open = None
+
+    def summary(self):
+        """{name: (launches, total bytes, total ms)} (call after synchronize)."""
+        out = {}
+        for name, nbytes, s, e in self.records:
+            c, b, t = out.get(name, (0, 0, 0.0))
+            out[name] = (c + 1, b + nbytes, t + s.elapsed_time(e))
+        return out
 
 
 def _prefix_host(degs, targets_np):
@@ -880,10 +935,26 @@ def resolve_budget(budget, resident_bytes=0):
     return budget
 
 
+def _exchange_for(distributed, mode, g):
+    """RowExchange when running full-mode inference across torch.distributed ranks."""
+    if distributed is False or mode != "full":
+        return None
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        if distributed is True:
+            raise ConfigError("distributed=True needs an initialised process group")
+        return None
+    from .parallel import RowExchange, edge_balanced_ranges
+
+    world = dist.get_world_size()
+    return RowExchange(edge_balanced_ranges(g.indptr_host, world), dist.get_rank(), world)
+
+
 def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanout=None, seed=0,
                   executor="layerwise", order="none", budget=None, thresholds=None,
                   batch_size=1024, store_backing="memory", workdir=None, output="auto",
-                  precision=None) -> InferenceResult:
+                  precision=None, distributed="auto") -> InferenceResult:
     """End to end: reorder, annotate, execute, de-permute (glint/executor.py:481-543).
 
     ``budget`` may be a DeviceBudget (reference behaviour) or ``"device"``:
@@ -891,6 +962,10 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     ``output``: "numpy", "device" or "auto" (numpy when the features came
     from the host).  ``store_backing="file"`` is accepted for compatibility;
     stores stay HBM-resident either way (outputs are identical).
+    ``distributed``: "auto" row-partitions full-mode layer-wise inference over
+    an initialised torch.distributed group (one process per GPU, NCCL); each
+    rank computes its edge-balanced node range and returns the full output.
+    Batch records / stats then describe the calling rank's own batches.
     """
     import torch
 
@@ -935,8 +1010,12 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     if executor == "layerwise":
         schedule = split(m)
         bud = resolve_budget(budget, _resident_bytes(m, schedule, tsets, g_i))
-        eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision)
-        store = eng.run()
+        ex = _exchange_for(distributed, mode, g_i)
+        eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision,
+                              row_range=ex.row_range if ex else None)
+        store = eng.run(exchange=ex)
+        if ex is not None:
+            ex.exchange_tensor(store.data)      # every rank returns the full output
         row_ids = tsets.v_sets[m.depth if m.depth else 0]
         out_dev = _gather_rows(store, row_ids, node_order.inv[user_targets], dg0.device)
     else:
@@ -945,9 +1024,14 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
                                     sampled=tsets.sampled, precision=precision)
         row_ids = internal
         out_dev = _gather_dense(out_sorted, row_ids, node_order.inv[user_targets])
+    if host_out:
+        staging = torch.empty(tuple(out_dev.shape), dtype=torch.float32, pin_memory=True)
+        staging.copy_(out_dev)
+        output_val = staging.numpy()
+    else:
+        output_val = out_dev
     torch.cuda.synchronize(dg0.device)
     stats.wall_time = time.perf_counter() - started
-    output_val = out_dev.cpu().numpy() if host_out else out_dev
     return InferenceResult(output=output_val, target_ids=user_targets, stats=stats,
                            order=node_order, schedule=schedule, budget=bud)
 

@@ -1,0 +1,75 @@
+"""Multi-process (gloo, world_size 2/3) checks of the row partition and exchange."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2211_15082_b200.parallel import RowExchange, edge_balanced_ranges
+
+
+def test_edge_balanced_ranges_cover_once_and_balance():
+    rng = np.random.default_rng(0)
+    degs = rng.zipf(2.0, size=10000).clip(max=3000)
+    indptr = np.zeros(10001, dtype=np.int64)
+    np.cumsum(degs, out=indptr[1:])
+    for parts in (1, 2, 3, 4, 8):
+        cuts = edge_balanced_ranges(indptr, parts)
+        assert cuts[0] == 0 and cuts[-1] == 10000 and np.all(np.diff(cuts) >= 0)
+        cost = np.diff(indptr + np.arange(10001))
+        loads = [cost[cuts[k]:cuts[k + 1]].sum() for k in range(parts)]
+        assert max(loads) <= cost.sum() / parts + cost.max()
+
+
+def test_edge_balanced_ranges_degenerate():
+    assert edge_balanced_ranges(np.zeros(1, dtype=np.int64), 4).tolist() == [0, 0, 0, 0, 0]
+    assert edge_balanced_ranges(np.array([0, 5]), 2).tolist()[-1] == 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, dim, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    indptr = np.arange(n + 1, dtype=np.int64) * 3
+    cuts = edge_balanced_ranges(indptr, world)
+    ex = RowExchange(cuts, rank, world)
+    data = torch.full((n, dim), -1.0)
+    lo, hi = ex.row_range
+    # each rank "computes" its rows: value = row id * 10 + column
+    rows = torch.arange(lo, hi, dtype=torch.float32)[:, None] * 10 + torch.arange(dim)[None, :]
+    data[lo:hi] = rows
+    ex.exchange_tensor(data)
+    want = torch.arange(n, dtype=torch.float32)[:, None] * 10 + torch.arange(dim)[None, :]
+    result_q.put((rank, bool(torch.equal(data, want)), ex.bytes_sent, (lo, hi)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 37, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _, _ in results)
+    covered = sorted(r for _, _, _, r in results)
+    assert covered[0][0] == 0 and covered[-1][1] == 37
+    assert sum(b for _, _, b, _ in results) == 37 * 5 * 4
