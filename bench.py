@@ -432,7 +432,9 @@ def run_e2e(args, m, g, xt, budget, world, rank, ex):
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    res = None
     for _ in range(steps):
+        res = None      # the caller is done with the previous result (recycles pinned staging)
         res = run_inference(m, host_graph, xh, budget=budget, output="numpy")
     torch.cuda.synchronize()
     barrier(world)

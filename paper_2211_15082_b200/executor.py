@@ -140,7 +140,9 @@ def annotate(g, targets, depth, mode, fanout=None, seed=0) -> TargetSets:
     if mode not in MODES:
         raise ConfigError(f"unknown inference mode {mode!r}")
     n = g.num_nodes
-    targets = np.unique(np.asarray(targets, dtype=np.int64))
+    targets = np.asarray(targets, dtype=np.int64)
+    if not (mode == "full" and len(targets) == n and _is_arange(targets)):
+        targets = np.unique(targets)
     if len(targets) and (targets[0] < 0 or targets[-1] >= n):
         raise ConfigError("target ids out of range")
     sampled = None
@@ -998,7 +1000,10 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     dg0 = kernels.device_graph(g)
     x0 = _as_device_store(x_store, dg0.device)
     g_i, x_i = apply_order_device(dg0, x0, node_order)
-    internal = np.sort(node_order.inv[user_targets]) if len(user_targets) else user_targets
+    if mode == "full" or targets is None:
+        internal = user_targets                      # sorted(inv[arange(N)]) == arange(N)
+    else:
+        internal = np.sort(node_order.inv[user_targets]) if len(user_targets) else user_targets
     thresholds = thresholds or Thresholds(n_t=1024, n_i=32768)
     stats = RunStats(executor=executor, mode=mode, order=order, depth=m.depth,
                      initial_thresholds=(thresholds.n_t, thresholds.n_i)
@@ -1053,10 +1058,26 @@ def _resident_bytes(m, schedule, tsets, g):
     return peak
 
 
+def _is_arange(a) -> bool:
+    """a == arange(len(a)) (cheap checks first)."""
+    n = len(a)
+    return n == 0 or (a[0] == 0 and a[-1] == n - 1 and bool(np.all(np.diff(a) == 1)))
+
+
 def _gather_rows(store: DeviceStore, row_ids, wanted, device):
     """Rows of `store` (rows = sorted row_ids) for internal ids `wanted`, in order."""
     import torch
 
+    if len(row_ids) == store.num_rows and _is_arange(row_ids):
+        if _is_arange(wanted) and len(wanted) == store.num_rows:
+            return store.view()                      # identity: no gather needed
+        if len(wanted) and (wanted.min() < 0 or wanted.max() >= store.num_rows):
+            raise InternalError("output rows do not cover the requested targets")
+        out = torch.empty((len(wanted), store.dim), dtype=torch.float32, device=device)
+        if len(wanted):
+            kernels.copy_rows(out, store.view(),
+                              src_rows=torch.from_numpy(np.ascontiguousarray(wanted)).to(device))
+        return out
     pos = np.searchsorted(row_ids, wanted)
     if len(wanted):
         safe = np.minimum(pos, len(row_ids) - 1)

@@ -36,7 +36,7 @@ class NodeOrder:
     def __post_init__(self):
         perm = np.ascontiguousarray(self.perm, dtype=np.int64)
         n = len(perm)
-        if n:
+        if n and not (perm[0] == 0 and perm[-1] == n - 1 and np.all(np.diff(perm) == 1)):
             seen = np.zeros(n, dtype=bool)
             ok = perm.min() >= 0 and perm.max() < n
             if ok:

@@ -210,6 +210,41 @@ def test_linear_row_invariance(cuda):
     assert rel_l2(full, orc.linear(x, w, b)) <= 1e-6
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 47, 100), (300, 47, 100), (1000, 256, 256),
+                                   (129, 300, 64), (257, 16, 3), (4096, 128, 128),
+                                   (77, 48, 188), (5000, 256, 100)])
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_tcgen05_3xtf32_linear(cuda, M, N, K, act):
+    """Tensor-core split-TF32 GEMM vs fp64: rel-L2 <= 1e-6 (plain TF32 would be ~3e-4),
+    bias + activation epilogue, row gather, M/N/K tails, N > 256 (two column tiles)."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(M * 7 + N + K + act)
+    x = rng.normal(size=(M + 5, K)).astype(np.float32)
+    w = (rng.normal(size=(N, K)) / np.sqrt(K)).astype(np.float32)
+    b = rng.normal(size=N).astype(np.float32)
+    rows = rng.permutation(M + 5)[:M].astype(np.int64)
+    want = x[rows].astype(np.float64) @ w.T.astype(np.float64) + b
+    if act == 1:
+        want = np.maximum(want, 0)
+    elif act == 2:
+        want = np.where(want >= 0, want, 0.2 * want)
+    xd, wd, bd = (torch.from_numpy(a).cuda() for a in (x, w, b))
+    rd = torch.from_numpy(rows).cuda()
+    base = torch.full((M, N + 3), 7.0, device="cuda")
+    out = base[:, :N]
+    kernels.linear_into(out, xd, wd, bd, act, a_rows=rd, precision=_lib.PREC_3XTF32)
+    got = out.cpu().numpy()
+    assert rel_l2(got, want) <= 1e-6, rel_l2(got, want)
+    assert torch.all(base[:, N:] == 7.0)             # no writes past N
+    # row invariance on the tensor cores
+    one = torch.empty((1, N), device="cuda")
+    kernels.linear_into(one, xd, wd, bd, act, a_rows=rd[M // 2:M // 2 + 1], precision=_lib.PREC_3XTF32)
+    assert one.cpu().numpy().tobytes() == got[M // 2:M // 2 + 1].tobytes()
+
+
 def test_shape_errors_are_value_errors(cuda):
     from paper_2211_15082_b200 import kernels
 
