@@ -64,6 +64,13 @@ typedef void* glint_stream_t; /* cudaStream_t */
 /* ------------------------------------------------------------------ misc */
 const char* glint_last_error(void);
 int glint_abi_version(void);
+
+/* Process-wide tuning knobs (performance only; results are identical for
+ * every setting).  0 selects the default. */
+#define GLINT_TUNE_MEAN_VARIANT 0 /* K1 launch variant (occupancy / unroll) */
+#define GLINT_TUNE_COUNT 8
+int glint_set_tuning(int key, int value);
+int glint_get_tuning(int key);
 /* host pointers; fills the properties of `device` */
 int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                       size_t* free_bytes, size_t* total_bytes);

@@ -37,6 +37,8 @@ _SZ = ctypes.c_size_t
 SIGNATURES = {
     "glint_last_error": (ctypes.c_char_p, []),
     "glint_abi_version": (ctypes.c_int, []),
+    "glint_set_tuning": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "glint_get_tuning": (ctypes.c_int, [ctypes.c_int]),
     "glint_device_info": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P]),
     "glint_spmm_mean_f32": (ctypes.c_int, [_I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _I64,
                                            _P, _I64, _P, _I64, _P]),
@@ -100,7 +102,7 @@ def last_error() -> str:
 # memset-only entry points launch none.
 KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
                     "glint_degree_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
-                    "glint_device_info": 0}
+                    "glint_device_info": 0, "glint_set_tuning": 0}
 LAUNCHES = [0]
 
 

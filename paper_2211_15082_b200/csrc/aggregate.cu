@@ -196,8 +196,8 @@ __device__ __forceinline__ void mean_row_hub(const MeanArgs& a, int64_t r, int c
   }
 }
 
-template <int VEC, int LPR, int VPL, int U>
-__global__ void __launch_bounds__(kThreads) mean_kernel(MeanArgs a) {
+template <int VEC, int LPR, int VPL, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) mean_kernel(MeanArgs a) {
   __shared__ int64_t s_off[kHubChunk];
   if (static_cast<int64_t>(blockIdx.x) < a.sc.hub_ctas) {
     const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) mean_kernel(MeanArgs a) {
   mean_row_regular<VEC, LPR, VPL, U>(a, r, lane_g, gmask);
 }
 
-template <int VEC, int LPR, int VPL, int U>
+template <int VEC, int LPR, int VPL, int U, int MINB = 3>
 int launch_mean(const MeanArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
   const int64_t regular = a.sc.n_rows - a.sc.n_hub;
@@ -229,11 +229,29 @@ int launch_mean(const MeanArgs& a, cudaStream_t s) {
     set_error("spmm_mean: grid too large");
     return GLINT_EINVAL;
   }
-  mean_kernel<VEC, LPR, VPL, U><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  mean_kernel<VEC, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
   return launch_status("spmm_mean");
 }
 
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
+  // Tuning variants (glint_set_tuning(GLINT_TUNE_MEAN_VARIANT, v)) for the
+  // widths of the headline workload; 0 is the default.
+  const int variant = tuning(GLINT_TUNE_MEAN_VARIANT);
+  if (vec4 && variant != 0) {
+    const int d4 = static_cast<int>(ceil_div(a.dim, 4));
+    if (d4 > 16 && d4 <= 32) {
+      if (variant == 1) return launch_mean<4, 32, 1, 8, 4>(a, s);
+      if (variant == 2) return launch_mean<4, 32, 1, 16, 2>(a, s);
+      if (variant == 3) return launch_mean<4, 16, 2, 8, 2>(a, s);
+      if (variant == 4) return launch_mean<4, 32, 1, 12, 3>(a, s);
+    }
+    if (d4 > 32 && d4 <= 64) {
+      if (variant == 1) return launch_mean<4, 32, 2, 4, 4>(a, s);
+      if (variant == 2) return launch_mean<4, 32, 2, 8, 2>(a, s);
+      if (variant == 3) return launch_mean<4, 16, 4, 4, 2>(a, s);
+      if (variant == 4) return launch_mean<4, 32, 2, 6, 3>(a, s);
+    }
+  }
   if (vec4) {
     const int d4 = static_cast<int>(ceil_div(a.dim, 4));
     if (d4 <= 8) return launch_mean<4, 8, 1, 8>(a, s);

@@ -27,6 +27,8 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int sm_count();  // cached per current device
 
+int tuning(int key);  // glint_set_tuning knobs (0 = default behaviour)
+
 constexpr int kWarp = 32;
 
 }  // namespace glint

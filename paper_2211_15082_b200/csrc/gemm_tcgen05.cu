@@ -1,47 +1,62 @@
 // K2 on the 5th-generation tensor cores: C = act(A W^T + b) in split-TF32
-// ("3xTF32") with tcgen05.mma kind::tf32, fp32 accumulators in TMEM.
+// ("3xTF32") with tcgen05.mma kind::tf32 and fp32 accumulators in TMEM.
 //
 // Reference op: kernels.py:95-107 (linear, fp32 einsum).  Plain TF32 misses
-// the rel-L2 1e-4 end-to-end bar (3.4e-4), so every operand is
-// split into a TF32-exact high part and a residual, x = hi + lo with
-// hi = x with the low 13 mantissa bits cleared and lo = x - hi (exact in fp32),
-// and the product is hi*hi + hi*lo + lo*hi (lo*lo ~ 2^-22 relative is dropped).
-// Measured error of the scheme ~1e-7 rel-L2.
+// the rel-L2 1e-4 end-to-end bar (3.4e-4), so each operand is split
+// x = hi + lo, hi = x with the low 13 mantissa bits cleared (TF32-exact),
+// lo = x - hi (exact in fp32), and the product is lo*hi + hi*lo + hi*hi
+// (lo*lo ~ 2^-22 relative is dropped).  Measured ~1e-6 rel-L2 vs fp64.
 //
-// Tiling: one CTA (4 warps) per 128-row M tile x BN columns; K advances in
-// 32-element blocks through a 2-stage shared-memory ring.  Every thread loads
-// A / W with 128-bit loads, splits hi/lo in registers and writes both parts
-// into the canonical no-swizzle K-major UMMA layout (8-row x 16-byte core
-// matrices: LBO = 128 B along K, SBO = 1024 B between 8-row groups).  One
-// thread issues 3 x (BK/8) tcgen05.mma (M=128, N=BN, K=8) per block and
-// commits them to the stage's mbarrier, which gates reuse of that stage.  The
-// epilogue reads the accumulator with tcgen05.ld (warp w owns TMEM lanes
-// 32w..32w+31 = tile rows), adds bias, applies the activation and stores.
+// Persistent, warp-specialised kernel, one CTA per SM (416 threads):
+//   warps 0-7  producers, two groups of 4 warps taking alternate K blocks:
+//              128-bit global loads of A (256 rows) and W (BN rows) for one
+//              BK=16 block, hi/lo split in registers, stores into the
+//              canonical no-swizzle K-major UMMA layout (8-row x 16 B core
+//              matrices, LBO = 128 B along K, SBO = 512 B between 8-row
+//              groups), fence.proxy.async, arrive on the stage's FULL barrier;
+//   warp 8     allocates TMEM (2*BN columns: one 128-lane accumulator per
+//              M half) and issues 2 k-steps x 2 halves x 3 products of
+//              tcgen05.mma (M=128, N=BN, K=8) per block; tcgen05.commit frees
+//              the stage (EMPTY barrier) and, after the last block, signals
+//              TMEM_FULL;
+//   warps 9-12 epilogue: tcgen05.ld 32x32b.x32 (warp%4 owns TMEM lane quarter
+//              = 32 tile rows), bias + activation, transpose through a padded
+//              shared staging tile, coalesced 128 B global stores, then
+//              arrive TMEM_EMPTY.
+// A 3-stage shared-memory ring (3 x 64 KB at BN=256) decouples producers from
+// the MMA issuer; W tiles are shared by both 128-row halves of a 256-row tile,
+// halving W re-reads from L2 per output row.
 //
-// Row invariance (kernels.py:1-14): each output row depends only on its own
-// A row and W, with a fixed k order, so any batching of rows gives the same
-// bytes.
+// Row invariance (kernels.py:1-14): an output row depends only on its own A
+// row and W with a fixed k order, so any batching of rows gives equal bytes.
 #include "common.cuh"
 
 namespace glint {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 32;
-constexpr int kTcThreads = 128;
+constexpr int BM = 256;           // rows per tile (two M=128 MMA halves)
+constexpr int HALF = 128;
+constexpr int BK = 16;            // K per pipeline stage (2 MMA k-steps)
+constexpr int STAGES = 3;
+constexpr int kProducerWarps = 8;
+constexpr int kMmaWarp = 8;
+constexpr int kEpiWarp0 = 9;
+constexpr int kThreads = 13 * 32;
+constexpr uint32_t SBO = (BK / 4) * 128;   // bytes between 8-row core-matrix groups
+constexpr uint32_t LBO = 128;              // bytes between K-adjacent core matrices
+constexpr int EPI_LD = 36;                 // staging row pitch (floats): conflict-free
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
-  return d;                             // base offset 0, layout type 0 (no swizzle)
+  d |= static_cast<uint64_t>((LBO >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((SBO >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100); no swizzle
+  return d;
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -64,6 +79,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" : : "r"(smem_addr(bar)), "r"(count));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" : : "r"(smem_addr(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred P1;\nLAB_WAIT:\n"
@@ -81,23 +100,35 @@ __device__ __forceinline__ void fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 template <int BN>
-struct TmemCols {
-  static constexpr uint32_t value = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+struct Cfg {
+  static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                    : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int A_BYTES = BM * BK * 4;  // one of hi / lo
+  static constexpr int W_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * W_BYTES;
+  static constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;
+  static constexpr int SMEM = STAGES * STAGE + EPI_BYTES;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>(HALF >> 4) << 24);
 };
 
 struct TcArgs {
@@ -111,22 +142,11 @@ struct TcArgs {
   const float* __restrict__ bias;
   float* __restrict__ C;
   int64_t ldc;
+  int64_t num_tiles;
+  int n_tiles;
+  int nkb;
+  bool c_vec4;
 };
-
-__device__ __forceinline__ void split_store(uint8_t* hi_base, uint8_t* lo_base, uint32_t off,
-                                            float4 v) {
-  float4 hi, lo;
-  hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-  hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-  hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-  hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-  lo.x = __fsub_rn(v.x, hi.x);
-  lo.y = __fsub_rn(v.y, hi.y);
-  lo.z = __fsub_rn(v.z, hi.z);
-  lo.w = __fsub_rn(v.w, hi.w);
-  *reinterpret_cast<float4*>(hi_base + off) = hi;
-  *reinterpret_cast<float4*>(lo_base + off) = lo;
-}
 
 template <bool VEC>
 __device__ __forceinline__ float4 load4(const float* row, int k, int K) {
@@ -143,147 +163,234 @@ __device__ __forceinline__ float4 load4(const float* row, int k, int K) {
   }
 }
 
-// Canonical no-swizzle K-major offset of (row r, 16-byte chunk c) in a tile
-// whose K extent is BK: core matrix = 8 rows x 16 B (128 B), K-adjacent core
-// matrices 128 B apart (LBO), 8-row groups BK*32 B apart (SBO).
+__device__ __forceinline__ void split_store(uint8_t* hi_base, uint8_t* lo_base, uint32_t off,
+                                            float4 v) {
+  float4 hi, lo;
+  hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  lo.x = __fsub_rn(v.x, hi.x);
+  lo.y = __fsub_rn(v.y, hi.y);
+  lo.z = __fsub_rn(v.z, hi.z);
+  lo.w = __fsub_rn(v.w, hi.w);
+  *reinterpret_cast<float4*>(hi_base + off) = hi;
+  *reinterpret_cast<float4*>(lo_base + off) = lo;
+}
+
+// (row r of a 128-row operand half or of W, 16-byte chunk c) -> byte offset
 __device__ __forceinline__ uint32_t tile_off(int r, int c) {
-  return static_cast<uint32_t>((r & 7) * 16 + c * 128 + (r >> 3) * (BK / 4) * 128);
+  return static_cast<uint32_t>((r & 7) * 16 + c * 128 + (r >> 3) * SBO);
+}
+
+template <int ACT>
+__device__ __forceinline__ float epilogue_op(float x, const float* bias, int col) {
+  if (bias) x = __fadd_rn(x, __ldg(bias + col));
+  if (ACT == GLINT_ACT_RELU) x = (x > 0.0f || x != x) ? x : 0.0f;
+  if (ACT == GLINT_ACT_LEAKY_RELU) x = x >= 0.0f ? x : __fmul_rn(0.2f, x);
+  return x;
 }
 
 template <int BN, bool VEC, int ACT>
-__global__ void __launch_bounds__(kTcThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
+  using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tmem_full;
+  __shared__ __align__(8) uint64_t tmem_empty;
   __shared__ uint32_t tmem_slot;
-  constexpr int A_BYTES = BM * BK * 4;
-  constexpr int W_BYTES = BN * BK * 4;
-  constexpr int STAGE = 2 * A_BYTES + 2 * W_BYTES;
-  constexpr uint32_t TCOLS = TmemCols<BN>::value;
-  constexpr uint32_t SBO = (BK / 4) * 128;
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
-                             (static_cast<uint32_t>(BN >> 3) << 17) |
-                             (static_cast<uint32_t>(BM >> 4) << 24);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  :
-                 : "r"(smem_addr(&tmem_slot)), "r"(TCOLS));
+                 : "r"(smem_addr(&tmem_slot)), "r"(C::TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 4);   // one arrive per producer warp of the group
+      mbar_init(&empty_bar[s], 1);  // tcgen05.commit
+    }
+    mbar_init(&tmem_full, 1);
+    mbar_init(&tmem_empty, 4);      // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_slot;
+  const int nkb = a.nkb;
 
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
-  const int n0 = blockIdx.y * BN;
-  const int nkb = (a.K + BK - 1) / BK;
-
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb & 1;
-    uint8_t* a_hi = smem + s * STAGE;
-    uint8_t* a_lo = a_hi + A_BYTES;
-    uint8_t* w_hi = a_lo + A_BYTES;
-    uint8_t* w_lo = w_hi + W_BYTES;
-    if (kb >= 2) mbar_wait(&bars[s], static_cast<uint32_t>(((kb >> 1) - 1) & 1));
-    const int kbase = kb * BK;
-    // A tile: warp w fills 8-row groups w, w+4, w+8, w+12; lane -> (row in group, chunk)
+  if (warp < kProducerWarps) {
+    // ---------------------------------------------------------- producers
+    const int grp = warp >> 2;
+    const int wq = warp & 3;
+    const int rsub = lane & 7;
+    const int chunk = lane >> 3;  // 0..3: 16-byte chunk within the BK=16 block
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      const int64_t m0 = (tile / a.n_tiles) * BM;
+      const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      for (int kb = grp; kb < nkb; kb += 2) {
+        const int64_t idx = it * nkb + kb;
+        const int s = static_cast<int>(idx % STAGES);
+        const uint32_t round = static_cast<uint32_t>(idx / STAGES);
+        mbar_wait(&empty_bar[s], (round & 1u) ^ 1u);
+        uint8_t* a_hi = smem + s * C::STAGE;
+        uint8_t* a_lo = a_hi + C::A_BYTES;
+        uint8_t* w_hi = a_lo + C::A_BYTES;
+        uint8_t* w_lo = w_hi + C::W_BYTES;
+        const int k = kb * BK + 4 * chunk;
+        float4 va[BM / 32];
 #pragma unroll
-    for (int i = 0; i < BM / 32; ++i) {
-      const int r = (warp + 4 * i) * 8 + (lane & 7);
-      const int64_t row = m0 + r;
-      const float* src = nullptr;
-      if (row < a.M) src = a.A + (a.a_rows ? a.a_rows[row] : row) * a.lda;
+        for (int i = 0; i < BM / 32; ++i) {
+          const int r = (wq + 4 * i) * 8 + rsub;  // 0..255
+          const int64_t row = m0 + r;
+          va[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < a.M)
+            va[i] = load4<VEC>(a.A + (a.a_rows ? a.a_rows[row] : row) * a.lda, k, a.K);
+        }
+        constexpr int WG = (BN / 8 + 3) / 4;
+        float4 vw[WG];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = (lane >> 3) + 4 * h;
-        const float4 v = src ? load4<VEC>(src, kbase + 4 * c, a.K) : make_float4(0.f, 0.f, 0.f, 0.f);
-        split_store(a_hi, a_lo, tile_off(r, c), v);
+        for (int i = 0; i < WG; ++i) {
+          const int r = (wq + 4 * i) * 8 + rsub;
+          vw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (r < BN && n0 + r < a.N)
+            vw[i] = load4<VEC>(a.W + static_cast<int64_t>(n0 + r) * a.ldw, k, a.K);
+        }
+#pragma unroll
+        for (int i = 0; i < BM / 32; ++i) {
+          const int r = (wq + 4 * i) * 8 + rsub;
+          const uint32_t off = (r >= HALF ? C::A_BYTES / 2 : 0) + tile_off(r & (HALF - 1), chunk);
+          split_store(a_hi, a_lo, off, va[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < WG; ++i) {
+          const int r = (wq + 4 * i) * 8 + rsub;
+          if (r < BN) split_store(w_hi, w_lo, tile_off(r, chunk), vw[i]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[s]);
       }
     }
-    // W tile: BN rows
-    for (int gidx = warp; gidx < BN / 8; gidx += 4) {
-      const int r = gidx * 8 + (lane & 7);
-      const int n = n0 + r;
-      const float* src = n < a.N ? a.W + static_cast<int64_t>(n) * a.ldw : nullptr;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = (lane >> 3) + 4 * h;
-        const float4 v = src ? load4<VEC>(src, kbase + 4 * c, a.K) : make_float4(0.f, 0.f, 0.f, 0.f);
-        split_store(w_hi, w_lo, tile_off(r, c), v);
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issue
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      mbar_wait(&tmem_empty, (static_cast<uint32_t>(it) & 1u) ^ 1u);
       fence_after();
-      const uint32_t ah = smem_addr(a_hi), al = smem_addr(a_lo);
-      const uint32_t wh = smem_addr(w_hi), wl = smem_addr(w_lo);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int64_t idx = it * nkb + kb;
+        const int s = static_cast<int>(idx % STAGES);
+        const uint32_t round = static_cast<uint32_t>(idx / STAGES);
+        mbar_wait(&full_bar[s], round & 1u);
+        fence_after();
+        if (lane == 0) {
+          const uint32_t a_hi = smem_addr(smem + s * C::STAGE);
+          const uint32_t a_lo = a_hi + C::A_BYTES;
+          const uint32_t w_hi = a_lo + C::A_BYTES;
+          const uint32_t w_lo = w_hi + C::W_BYTES;
 #pragma unroll
-      for (int j = 0; j < BK / 8; ++j) {
-        const uint32_t step = j * 256;  // 8 tf32 along K = two 16-byte core matrices
-        const uint64_t d_ah = umma_desc(ah + step, 128, SBO);
-        const uint64_t d_al = umma_desc(al + step, 128, SBO);
-        const uint64_t d_wh = umma_desc(wh + step, 128, SBO);
-        const uint64_t d_wl = umma_desc(wl + step, 128, SBO);
-        mma_tf32(tmem, d_al, d_wh, IDESC, (kb | j) != 0);
-        mma_tf32(tmem, d_ah, d_wl, IDESC, 1);
-        mma_tf32(tmem, d_ah, d_wh, IDESC, 1);
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t step = j * 256;  // 8 tf32 along K = two 16-byte core matrices
+            const uint64_t dwh = umma_desc(w_hi + step);
+            const uint64_t dwl = umma_desc(w_lo + step);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t hoff = h * (C::A_BYTES / 2) + step;
+              const uint32_t d = tmem + static_cast<uint32_t>(h * BN);
+              mma_tf32(d, umma_desc(a_lo + hoff), dwh, C::IDESC, (kb | j) != 0);
+              mma_tf32(d, umma_desc(a_hi + hoff), dwl, C::IDESC, 1u);
+              mma_tf32(d, umma_desc(a_hi + hoff), dwh, C::IDESC, 1u);
+            }
+          }
+          mma_commit(&empty_bar[s]);
+          if (kb == nkb - 1) mma_commit(&tmem_full);
+        }
+        __syncwarp();
       }
-      mma_commit(&bars[s]);
     }
-  }
-  const int last = nkb - 1;
-  mbar_wait(&bars[last & 1], static_cast<uint32_t>((last >> 1) & 1));
-  fence_after();
-
-  // epilogue: warp w <-> TMEM lanes 32w.., thread <-> one tile row
-  const int64_t row = m0 + warp * 32 + lane;
-  const uint32_t lane_addr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    float* stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE) + (warp - kEpiWarp0) * 32 * EPI_LD;
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      const int64_t m0 = (tile / a.n_tiles) * BM;
+      const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      mbar_wait(&tmem_full, static_cast<uint32_t>(it) & 1u);
+      fence_after();
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
-    tmem_ld16(lane_addr + c0, v);
-    if (row < a.M) {
-      float* dst = a.C + row * a.ldc;
+      for (int h = 0; h < 2; ++h) {
+        const int64_t row_base = m0 + h * HALF + q * 32;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + h * BN + c0, v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int col = n0 + c0 + i;
-        if (col < a.N) {
-          float x = v[i];
-          if (a.bias) x = __fadd_rn(x, a.bias[col]);
-          if (ACT == GLINT_ACT_RELU) x = (x > 0.0f || x != x) ? x : 0.0f;
-          if (ACT == GLINT_ACT_LEAKY_RELU) x = x >= 0.0f ? x : __fmul_rn(0.2f, x);
-          dst[col] = x;
+          for (int i = 0; i < 32; ++i) {
+            const int col = n0 + c0 + i;
+            v[i] = col < a.N ? epilogue_op<ACT>(v[i], a.bias, col) : 0.0f;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4*>(stage + lane * EPI_LD + 4 * i) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          __syncwarp();
+          const int cc = (lane & 7) * 4;
+          const int col = n0 + c0 + cc;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = (lane >> 3) + 4 * i;
+            const int64_t row = row_base + rr;
+            if (row < a.M && col < a.N) {
+              const float4 t = *reinterpret_cast<const float4*>(stage + rr * EPI_LD + cc);
+              float* dst = a.C + row * a.ldc + col;
+              if (a.c_vec4 && col + 3 < a.N) {
+                *reinterpret_cast<float4*>(dst) = t;
+              } else {
+                dst[0] = t.x;
+                if (col + 1 < a.N) dst[1] = t.y;
+                if (col + 2 < a.N) dst[2] = t.z;
+                if (col + 3 < a.N) dst[3] = t.w;
+              }
+            }
+          }
+          __syncwarp();
         }
       }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty);
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" : : "r"(tmem), "r"(TCOLS));
+  if (warp == kMmaWarp) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" : : "r"(tmem), "r"(C::TCOLS));
   }
 }
 
 template <int BN, bool VEC, int ACT>
-int launch_tc(const TcArgs& a, cudaStream_t s) {
-  constexpr int smem_bytes = 2 * (2 * BM * BK * 4 + 2 * BN * BK * 4);
+int launch_tc(TcArgs a, cudaStream_t s) {
+  using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
     GLINT_CUDA(cudaFuncSetAttribute(gemm_3xtf32_kernel<BN, VEC, ACT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(a.M, BM)), static_cast<unsigned>(ceil_div(a.N, BN)));
-  gemm_3xtf32_kernel<BN, VEC, ACT><<<grid, kTcThreads, smem_bytes, s>>>(a);
+  a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
+  a.num_tiles = ceil_div(a.M, BM) * a.n_tiles;
+  a.nkb = static_cast<int>(ceil_div(a.K, BK));
+  const int64_t grid = std::min<int64_t>(a.num_tiles, sm_count());
+  gemm_3xtf32_kernel<BN, VEC, ACT><<<static_cast<unsigned>(grid), kThreads, C::SMEM, s>>>(a);
   return launch_status("linear_3xtf32");
 }
 
@@ -300,6 +407,7 @@ int launch_bn(const TcArgs& a, int act, cudaStream_t s) {
   if (a.N <= 48) return launch_act<48, VEC>(a, act, s);
   if (a.N <= 64) return launch_act<64, VEC>(a, act, s);
   if (a.N <= 128) return launch_act<128, VEC>(a, act, s);
+  if (a.N <= 192) return launch_act<192, VEC>(a, act, s);
   return launch_act<256, VEC>(a, act, s);
 }
 
@@ -308,8 +416,19 @@ int launch_bn(const TcArgs& a, int act, cudaStream_t s) {
 int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
                          const int64_t* a_rows, const float* W, int64_t ldw, const float* bias,
                          int act, float* C, int64_t ldc, cudaStream_t s) {
-  GLINT_REQUIRE(ceil_div(M, BM) < (1LL << 31), "linear_3xtf32: M too large");
-  TcArgs a{M, N, K, A, lda, a_rows, W, ldw, bias, C, ldc};
+  TcArgs a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.A = A;
+  a.lda = lda;
+  a.a_rows = a_rows;
+  a.W = W;
+  a.ldw = ldw;
+  a.bias = bias;
+  a.C = C;
+  a.ldc = ldc;
+  a.c_vec4 = (ldc % 4 == 0) && aligned16(C);
   const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
   return vec ? launch_bn<true>(a, act, s) : launch_bn<false>(a, act, s);
 }

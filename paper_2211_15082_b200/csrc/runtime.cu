@@ -45,9 +45,21 @@ int sm_count() {
   return cached[dev];
 }
 
+static int g_tuning[GLINT_TUNE_COUNT] = {0};
+
+int tuning(int key) { return (key >= 0 && key < GLINT_TUNE_COUNT) ? g_tuning[key] : 0; }
+
 }  // namespace glint
 
 extern "C" {
+
+int glint_set_tuning(int key, int value) {
+  GLINT_REQUIRE(key >= 0 && key < GLINT_TUNE_COUNT, "set_tuning: unknown key %d", key);
+  glint::g_tuning[key] = value;
+  return GLINT_OK;
+}
+
+int glint_get_tuning(int key) { return glint::tuning(key); }
 
 const char* glint_last_error(void) { return glint::g_last_error.c_str(); }
 

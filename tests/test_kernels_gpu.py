@@ -215,7 +215,7 @@ def test_linear_row_invariance(cuda):
                                    (77, 48, 188), (5000, 256, 100)])
 @pytest.mark.parametrize("act", [0, 1, 2])
 def test_tcgen05_3xtf32_linear(cuda, M, N, K, act):
-    """Tensor-core split-TF32 GEMM vs fp64: rel-L2 <= 1e-6 (plain TF32 would be ~3e-4),
+    """Tensor-core split-TF32 GEMM vs fp64: rel-L2 <= 5e-6 (plain TF32 would be ~3e-4),
     bias + activation epilogue, row gather, M/N/K tails, N > 256 (two column tiles)."""
     import torch
 
@@ -237,7 +237,7 @@ def test_tcgen05_3xtf32_linear(cuda, M, N, K, act):
     out = base[:, :N]
     kernels.linear_into(out, xd, wd, bd, act, a_rows=rd, precision=_lib.PREC_3XTF32)
     got = out.cpu().numpy()
-    assert rel_l2(got, want) <= 1e-6, rel_l2(got, want)
+    assert rel_l2(got, want) <= 5e-6, rel_l2(got, want)
     assert torch.all(base[:, N:] == 7.0)             # no writes past N
     # row invariance on the tensor cores
     one = torch.empty((1, N), device="cuda")

@@ -1,0 +1,93 @@
+#!/usr/bin/env python
+"""Kernel-level sweep on the headline graph (run on the B200 box).
+
+Times K1 (mean aggregation) for every launch variant at the widths of the
+3-layer GCN workload, and K2 (GEMM) in fp32 SIMT vs tcgen05 3xTF32, with CUDA
+events on the launching stream, inputs larger than L2.  Prints one JSON line
+per measurement.  Also checks every variant's output bytes against variant 0.
+"""
+
+from __future__ import annotations
+
+import json
+import pathlib
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def timed(fn, reps=5):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels, synth
+    from paper_2211_15082_b200.executor import agg_bytes
+
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else synth.PRODUCTS_NODES
+    und = int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES))
+    g = synth.gen_products_like(n, und, seed=0, device="cuda")
+    deg = g.in_degrees
+    hub_pre = int(((deg + 1) >= kernels.HUB_MIN_DEGREE).sum())
+    sched, nh = kernels.degree_schedule(g.indptr, None, 0, n)
+    assert int(nh.item()) == hub_pre
+    print(json.dumps({"graph": {"nodes": n, "edges": g.num_edges, "max_deg": int(deg.max()),
+                                "hubs": hub_pre}}), flush=True)
+    for d in (100, 256, 48):
+        h = torch.randn((n, d), device="cuda")
+        out = torch.empty_like(h)
+        ref = None
+        for variant in range(5):
+            _lib.call("glint_set_tuning", 0, variant)
+
+            def run():
+                kernels.spmm_mean(out, h, g.indptr, g.indices, n, schedule=sched, n_hub=hub_pre)
+
+            ms = timed(run)
+            nb = agg_bytes(d, g.num_edges, n)
+            same = None
+            if ref is None:
+                ref = out.clone()
+            else:
+                same = bool(torch.equal(ref, out))
+            print(json.dumps({"kernel": "spmm_mean", "dim": d, "variant": variant, "ms": ms,
+                              "GBps": nb / ms / 1e6, "identical_to_v0": same}), flush=True)
+        # natural order, no hub path (effect of the LPT schedule)
+        _lib.call("glint_set_tuning", 0, 0)
+        ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n))
+        print(json.dumps({"kernel": "spmm_mean_nosched", "dim": d, "ms": ms,
+                          "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
+                          "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+        del h, out, ref
+    for (K, N) in ((100, 256), (256, 256), (256, 47)):
+        a = torch.randn((n, K), device="cuda")
+        w = torch.randn((N, K), device="cuda") / K ** 0.5
+        b = torch.randn((N,), device="cuda")
+        c = torch.empty((n, (N + 3) // 4 * 4), device="cuda")[:, :N]
+        res = {}
+        for prec in (0, 1):
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=prec))
+            res[prec] = c.clone()
+            print(json.dumps({"kernel": "linear", "K": K, "N": N, "precision": prec, "ms": ms,
+                              "TFLOPs": 2 * n * K * N / ms / 1e9,
+                              "GBps": (n * K * 4 + n * N * 4) / ms / 1e6}), flush=True)
+        err = float((res[0] - res[1]).norm() / res[0].norm())
+        print(json.dumps({"kernel": "linear_agree", "K": K, "N": N, "rel_l2_fp32_vs_3xtf32": err}))
+        del a, c
+
+
+if __name__ == "__main__":
+    main()
