@@ -236,28 +236,36 @@ int launch_mean(const MeanArgs& a, cudaStream_t s) {
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
   // Tuning variants (glint_set_tuning(GLINT_TUNE_MEAN_VARIANT, v)) for the
   // widths of the headline workload; 0 is the default.
+  // Measured on B200 (tools/sweep_kernels.py, profiles/): 4 CTAs/SM (<= 64
+  // registers) beats deeper unrolling at 2-3 CTAs/SM for d=100 and d=256.
   const int variant = tuning(GLINT_TUNE_MEAN_VARIANT);
   if (vec4 && variant != 0) {
     const int d4 = static_cast<int>(ceil_div(a.dim, 4));
+    if (d4 > 8 && d4 <= 16) {
+      if (variant == 1) return launch_mean<4, 8, 2, 8, 4>(a, s);
+      if (variant == 2) return launch_mean<4, 16, 1, 16, 3>(a, s);
+      if (variant == 3) return launch_mean<4, 4, 4, 8, 4>(a, s);
+      if (variant == 4) return launch_mean<4, 8, 2, 4, 6>(a, s);
+    }
     if (d4 > 16 && d4 <= 32) {
-      if (variant == 1) return launch_mean<4, 32, 1, 8, 4>(a, s);
+      if (variant == 1) return launch_mean<4, 32, 1, 8, 3>(a, s);
       if (variant == 2) return launch_mean<4, 32, 1, 16, 2>(a, s);
       if (variant == 3) return launch_mean<4, 16, 2, 8, 2>(a, s);
-      if (variant == 4) return launch_mean<4, 32, 1, 12, 3>(a, s);
+      if (variant == 4) return launch_mean<4, 32, 1, 4, 6>(a, s);
     }
     if (d4 > 32 && d4 <= 64) {
-      if (variant == 1) return launch_mean<4, 32, 2, 4, 4>(a, s);
+      if (variant == 1) return launch_mean<4, 32, 2, 4, 3>(a, s);
       if (variant == 2) return launch_mean<4, 32, 2, 8, 2>(a, s);
       if (variant == 3) return launch_mean<4, 16, 4, 4, 2>(a, s);
-      if (variant == 4) return launch_mean<4, 32, 2, 6, 3>(a, s);
+      if (variant == 4) return launch_mean<4, 32, 2, 2, 6>(a, s);
     }
   }
   if (vec4) {
     const int d4 = static_cast<int>(ceil_div(a.dim, 4));
-    if (d4 <= 8) return launch_mean<4, 8, 1, 8>(a, s);
-    if (d4 <= 16) return launch_mean<4, 16, 1, 8>(a, s);
-    if (d4 <= 32) return launch_mean<4, 32, 1, 8>(a, s);
-    if (d4 <= 64) return launch_mean<4, 32, 2, 4>(a, s);
+    if (d4 <= 8) return launch_mean<4, 8, 1, 8, 4>(a, s);
+    if (d4 <= 16) return launch_mean<4, 16, 1, 8, 4>(a, s);
+    if (d4 <= 32) return launch_mean<4, 32, 1, 8, 4>(a, s);
+    if (d4 <= 64) return launch_mean<4, 32, 2, 4, 4>(a, s);
     if (d4 <= 128) return launch_mean<4, 32, 4, 2>(a, s);
     return launch_mean<4, 32, 8, 2>(a, s);
   }

@@ -37,26 +37,40 @@ def main():
     from paper_2211_15082_b200 import _lib, kernels, synth
     from paper_2211_15082_b200.executor import agg_bytes
 
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else synth.PRODUCTS_NODES
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nodes", type=int, default=synth.PRODUCTS_NODES)
+    ap.add_argument("--what", default="spmm,gemm")
+    ap.add_argument("--dims", default="100,256,48")
+    ap.add_argument("--variants", type=int, default=5)
+    ap.add_argument("--gemm", default="100x256,256x256,256x47")
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    n = args.nodes
     und = int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES))
-    g = synth.gen_products_like(n, und, seed=0, device="cuda")
+    g = synth.gen_products_like(n, und, seed=0, device="cuda") if "spmm" in args.what else None
+    if g is None:
+        gemm_only(args, n)
+        return
     deg = g.in_degrees
     hub_pre = int(((deg + 1) >= kernels.HUB_MIN_DEGREE).sum())
     sched, nh = kernels.degree_schedule(g.indptr, None, 0, n)
     assert int(nh.item()) == hub_pre
     print(json.dumps({"graph": {"nodes": n, "edges": g.num_edges, "max_deg": int(deg.max()),
                                 "hubs": hub_pre}}), flush=True)
-    for d in (100, 256, 48):
+    dims = [int(x) for x in args.dims.split(",")] if "spmm" in args.what else []
+    for d in dims:
         h = torch.randn((n, d), device="cuda")
         out = torch.empty_like(h)
         ref = None
-        for variant in range(5):
+        for variant in range(args.variants):
             _lib.call("glint_set_tuning", 0, variant)
 
             def run():
                 kernels.spmm_mean(out, h, g.indptr, g.indices, n, schedule=sched, n_hub=hub_pre)
 
-            ms = timed(run)
+            ms = timed(run, args.reps)
             nb = agg_bytes(d, g.num_edges, n)
             same = None
             if ref is None:
@@ -72,14 +86,16 @@ def main():
                           "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
                           "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
         del h, out, ref
-    for (K, N) in ((100, 256), (256, 256), (256, 47)):
+    shapes = [tuple(int(v) for v in x.split("x")) for x in args.gemm.split(",")] \
+        if "gemm" in args.what else []
+    for (K, N) in shapes:
         a = torch.randn((n, K), device="cuda")
         w = torch.randn((N, K), device="cuda") / K ** 0.5
         b = torch.randn((N,), device="cuda")
         c = torch.empty((n, (N + 3) // 4 * 4), device="cuda")[:, :N]
         res = {}
         for prec in (0, 1):
-            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=prec))
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=prec), args.reps)
             res[prec] = c.clone()
             print(json.dumps({"kernel": "linear", "K": K, "N": N, "precision": prec, "ms": ms,
                               "TFLOPs": 2 * n * K * N / ms / 1e9,
@@ -87,6 +103,22 @@ def main():
         err = float((res[0] - res[1]).norm() / res[0].norm())
         print(json.dumps({"kernel": "linear_agree", "K": K, "N": N, "rel_l2_fp32_vs_3xtf32": err}))
         del a, c
+
+
+def gemm_only(args, n):
+    import torch
+
+    from paper_2211_15082_b200 import kernels
+
+    for x in args.gemm.split(","):
+        K, N = (int(v) for v in x.split("x"))
+        a = torch.randn((n, K), device="cuda")
+        w = torch.randn((N, K), device="cuda") / K ** 0.5
+        b = torch.randn((N,), device="cuda")
+        c = torch.empty((n, (N + 3) // 4 * 4), device="cuda")[:, :N]
+        ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
+        print(json.dumps({"kernel": "linear", "K": K, "N": N, "precision": 1, "ms": ms,
+                          "TFLOPs": 2 * n * K * N / ms / 1e9}), flush=True)
 
 
 if __name__ == "__main__":
