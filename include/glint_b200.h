@@ -68,9 +68,13 @@ int glint_abi_version(void);
 /* Process-wide tuning knobs (performance only; results are identical for
  * every setting).  0 selects the default. */
 #define GLINT_TUNE_MEAN_VARIANT 0 /* K1 launch variant (occupancy / unroll) */
+#define GLINT_TUNE_GEMM_PROF 1    /* 1: K2 tcgen05 kernel accumulates phase cycles */
 #define GLINT_TUNE_COUNT 8
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
+/* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of
+ * kernel family `which` (0 = tcgen05 GEMM). */
+int glint_debug_counters(int which, uint64_t* host_out, int n, int reset);
 /* host pointers; fills the properties of `device` */
 int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                       size_t* free_bytes, size_t* total_bytes);

@@ -39,6 +39,7 @@ SIGNATURES = {
     "glint_abi_version": (ctypes.c_int, []),
     "glint_set_tuning": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "glint_get_tuning": (ctypes.c_int, [ctypes.c_int]),
+    "glint_debug_counters": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int]),
     "glint_device_info": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P]),
     "glint_spmm_mean_f32": (ctypes.c_int, [_I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _I64,
                                            _P, _I64, _P, _I64, _P]),
@@ -102,7 +103,7 @@ def last_error() -> str:
 # memset-only entry points launch none.
 KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
                     "glint_degree_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
-                    "glint_device_info": 0, "glint_set_tuning": 0}
+                    "glint_device_info": 0, "glint_set_tuning": 0, "glint_debug_counters": 0}
 LAUNCHES = [0]
 
 

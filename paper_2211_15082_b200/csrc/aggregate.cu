@@ -246,18 +246,24 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
       if (variant == 2) return launch_mean<4, 16, 1, 16, 3>(a, s);
       if (variant == 3) return launch_mean<4, 4, 4, 8, 4>(a, s);
       if (variant == 4) return launch_mean<4, 8, 2, 4, 6>(a, s);
+      if (variant == 5) return launch_mean<4, 8, 2, 4, 8>(a, s);
+      if (variant == 6) return launch_mean<4, 16, 1, 4, 6>(a, s);
     }
     if (d4 > 16 && d4 <= 32) {
       if (variant == 1) return launch_mean<4, 32, 1, 8, 3>(a, s);
       if (variant == 2) return launch_mean<4, 32, 1, 16, 2>(a, s);
       if (variant == 3) return launch_mean<4, 16, 2, 8, 2>(a, s);
       if (variant == 4) return launch_mean<4, 32, 1, 4, 6>(a, s);
+      if (variant == 5) return launch_mean<4, 32, 1, 4, 8>(a, s);
+      if (variant == 6) return launch_mean<4, 32, 1, 6, 5>(a, s);
     }
     if (d4 > 32 && d4 <= 64) {
       if (variant == 1) return launch_mean<4, 32, 2, 4, 3>(a, s);
       if (variant == 2) return launch_mean<4, 32, 2, 8, 2>(a, s);
       if (variant == 3) return launch_mean<4, 16, 4, 4, 2>(a, s);
       if (variant == 4) return launch_mean<4, 32, 2, 2, 6>(a, s);
+      if (variant == 5) return launch_mean<4, 32, 2, 2, 8>(a, s);
+      if (variant == 6) return launch_mean<4, 32, 2, 3, 5>(a, s);
     }
   }
   if (vec4) {

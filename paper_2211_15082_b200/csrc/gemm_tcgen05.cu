@@ -146,7 +146,17 @@ struct TcArgs {
   int n_tiles;
   int nkb;
   bool c_vec4;
+  unsigned long long* prof;  // optional phase-cycle counters (GLINT_TUNE_GEMM_PROF)
 };
+
+// Phase counters, summed over CTAs: 0 producer wait(empty), 1 producer work,
+// 2 mma wait(full), 3 mma wait(tmem_empty), 4 epilogue wait(tmem_full),
+// 5 epilogue work, 6 kernel cycles, 7 tiles.
+__device__ unsigned long long g_gemm_prof[8];
+
+__device__ __forceinline__ void prof_add(const TcArgs& a, int k, unsigned long long v) {
+  if (a.prof) atomicAdd(a.prof + k, v);
+}
 
 template <bool VEC>
 __device__ __forceinline__ float4 load4(const float* row, int k, int K) {
@@ -201,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
   __shared__ __align__(8) uint64_t tmem_empty;
   __shared__ uint32_t tmem_slot;
 
+  const unsigned long long t_start = clock64();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp == kMmaWarp) {
@@ -230,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
     const int wq = warp & 3;
     const int rsub = lane & 7;
     const int chunk = lane >> 3;  // 0..3: 16-byte chunk within the BK=16 block
+    unsigned long long t_wait = 0, t_work = 0;
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
       const int64_t m0 = (tile / a.n_tiles) * BM;
@@ -238,7 +250,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
         const int64_t idx = it * nkb + kb;
         const int s = static_cast<int>(idx % STAGES);
         const uint32_t round = static_cast<uint32_t>(idx / STAGES);
+        const unsigned long long t0 = clock64();
         mbar_wait(&empty_bar[s], (round & 1u) ^ 1u);
+        const unsigned long long t1 = clock64();
+        t_wait += t1 - t0;
         uint8_t* a_hi = smem + s * C::STAGE;
         uint8_t* a_lo = a_hi + C::A_BYTES;
         uint8_t* w_hi = a_lo + C::A_BYTES;
@@ -276,19 +291,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_bar[s]);
+        t_work += clock64() - t1;
       }
+    }
+    if (lane == 0) {
+      prof_add(a, 0, t_wait);
+      prof_add(a, 1, t_work);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issue
+    unsigned long long t_full = 0, t_tmem = 0;
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      unsigned long long t0 = clock64();
       mbar_wait(&tmem_empty, (static_cast<uint32_t>(it) & 1u) ^ 1u);
+      t_tmem += clock64() - t0;
       fence_after();
       for (int kb = 0; kb < nkb; ++kb) {
         const int64_t idx = it * nkb + kb;
         const int s = static_cast<int>(idx % STAGES);
         const uint32_t round = static_cast<uint32_t>(idx / STAGES);
+        t0 = clock64();
         mbar_wait(&full_bar[s], round & 1u);
+        t_full += clock64() - t0;
         fence_after();
         if (lane == 0) {
           const uint32_t a_hi = smem_addr(smem + s * C::STAGE);
@@ -315,15 +340,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
         __syncwarp();
       }
     }
+    if (lane == 0) {
+      prof_add(a, 2, t_full);
+      prof_add(a, 3, t_tmem);
+      prof_add(a, 7, static_cast<unsigned long long>(it));
+    }
   } else {
     // ------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     float* stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE) + (warp - kEpiWarp0) * 32 * EPI_LD;
+    unsigned long long t_wait = 0, t_work = 0;
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
       const int64_t m0 = (tile / a.n_tiles) * BM;
       const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      const unsigned long long t0 = clock64();
       mbar_wait(&tmem_full, static_cast<uint32_t>(it) & 1u);
+      const unsigned long long t1 = clock64();
+      t_wait += t1 - t0;
       fence_after();
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
@@ -367,10 +401,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty);
+      t_work += clock64() - t1;
+    }
+    if (lane == 0) {
+      prof_add(a, 4, t_wait);
+      prof_add(a, 5, t_work);
     }
   }
   fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) prof_add(a, 6, clock64() - t_start);
   if (warp == kMmaWarp) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" : : "r"(tmem), "r"(C::TCOLS));
@@ -429,8 +469,25 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
   a.C = C;
   a.ldc = ldc;
   a.c_vec4 = (ldc % 4 == 0) && aligned16(C);
+  a.prof = nullptr;
+  if (tuning(GLINT_TUNE_GEMM_PROF)) {
+    void* p = nullptr;
+    GLINT_CUDA(cudaGetSymbolAddress(&p, g_gemm_prof));
+    a.prof = static_cast<unsigned long long*>(p);
+  }
   const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
   return vec ? launch_bn<true>(a, act, s) : launch_bn<false>(a, act, s);
 }
 
 }  // namespace glint
+
+extern "C" int glint_debug_counters(int which, uint64_t* host_out, int n, int reset) {
+  GLINT_REQUIRE(which == 0 && n >= 0 && n <= 8 && (host_out || n == 0),
+                "debug_counters: bad argument");
+  if (n) GLINT_CUDA(cudaMemcpyFromSymbol(host_out, glint::g_gemm_prof, n * sizeof(uint64_t)));
+  if (reset) {
+    const unsigned long long zeros[8] = {0};
+    GLINT_CUDA(cudaMemcpyToSymbol(glint::g_gemm_prof, zeros, sizeof(zeros)));
+  }
+  return GLINT_OK;
+}
