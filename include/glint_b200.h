@@ -93,13 +93,19 @@ int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
  * produced by glint_degree_schedule; its first n_hub entries are hub rows
  * processed cooperatively by a whole CTA (columns split across threads, so
  * the per-column summation order is unchanged).  Without a schedule rows run
- * in natural order and n_hub must be 0. */
+ * in natural order and n_hub must be 0.
+ * Optional epilogue (bias nullable, act = GLINT_ACT_*):
+ *   out = act(mean + bias[c]) -- used when a ConvMean is reassociated as
+ *   mean(h W^T) + b for layers that narrow the width (same math as
+ *   model_ir.py:336-338 up to fp32 rounding); bias=NULL, act=NONE is the
+ *   plain agg_mean. */
 int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
                         const int32_t* indices, const int64_t* row_ids,
                         int64_t row_base, const int64_t* self_rows,
                         const int32_t* col_map, const float* h, int64_t ld_h,
                         float* out, int64_t ld_out, const int32_t* schedule,
-                        int64_t n_hub, glint_stream_t stream);
+                        int64_t n_hub, const float* bias, int32_t act,
+                        glint_stream_t stream);
 
 /* Degree-bucketed longest-first schedule over n_rows output rows (CSR rows
  * as for glint_spmm_mean_f32).  Writes a permutation of [0, n_rows) to

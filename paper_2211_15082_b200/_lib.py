@@ -42,7 +42,7 @@ SIGNATURES = {
     "glint_debug_counters": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int]),
     "glint_device_info": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P]),
     "glint_spmm_mean_f32": (ctypes.c_int, [_I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _I64,
-                                           _P, _I64, _P, _I64, _P]),
+                                           _P, _I64, _P, _I64, _P, _I32, _P]),
     "glint_degree_schedule_workspace_bytes": (_SZ, []),
     "glint_degree_schedule": (ctypes.c_int, [_I64, _P, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "glint_linear_f32": (ctypes.c_int, [_I64, _I32, _I32, _P, _I64, _P, _P, _I64, _P, _I32,

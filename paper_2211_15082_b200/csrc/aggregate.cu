@@ -75,7 +75,16 @@ struct MeanArgs {
   int64_t ld_h;
   float* __restrict__ out;
   int64_t ld_out;
+  const float* __restrict__ bias;  // optional epilogue: act(mean + bias)
+  int act;
 };
+
+__device__ __forceinline__ float mean_epilogue(const MeanArgs& a, float v, int col) {
+  if (a.bias) v = __fadd_rn(v, __ldg(a.bias + col));
+  if (a.act == GLINT_ACT_RELU) v = (v > 0.0f || v != v) ? v : 0.0f;
+  if (a.act == GLINT_ACT_LEAKY_RELU) v = v >= 0.0f ? v : __fmul_rn(0.2f, v);
+  return v;
+}
 
 template <int VEC>
 __device__ __forceinline__ void load_vec(float (&v)[VEC], const float* p) {
@@ -155,7 +164,9 @@ __device__ __forceinline__ void mean_row_regular(const MeanArgs& a, int64_t r, i
         float s[VEC];
         load_vec<VEC>(s, a.h + self_off + col);
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) acc[k][c] = __fdiv_rn(__fadd_rn(acc[k][c], s[c]), degp1);
+        for (int c = 0; c < VEC; ++c)
+          acc[k][c] = mean_epilogue(a, __fdiv_rn(__fadd_rn(acc[k][c], s[c]), degp1),
+                                    col + c < a.dim ? col + c : col);
         store_vec<VEC>(a.out + r * a.ld_out + col, acc[k], a.dim - col);
       }
     }
@@ -192,7 +203,7 @@ __device__ __forceinline__ void mean_row_hub(const MeanArgs& a, int64_t r, int c
   }
   if (active) {
     acc = __fadd_rn(acc, __ldg(a.h + self_off + col));
-    a.out[r * a.ld_out + col] = __fdiv_rn(acc, degp1);
+    a.out[r * a.ld_out + col] = mean_epilogue(a, __fdiv_rn(acc, degp1), col);
   }
 }
 
@@ -268,10 +279,12 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
   }
   if (vec4) {
     const int d4 = static_cast<int>(ceil_div(a.dim, 4));
-    if (d4 <= 8) return launch_mean<4, 8, 1, 8, 4>(a, s);
-    if (d4 <= 16) return launch_mean<4, 16, 1, 8, 4>(a, s);
-    if (d4 <= 32) return launch_mean<4, 32, 1, 8, 4>(a, s);
-    if (d4 <= 64) return launch_mean<4, 32, 2, 4, 4>(a, s);
+    // Defaults = best measured variants (profiles/r01_spmm_sweep.jsonl):
+    // d=48 4102 GB/s, d=100 4898 GB/s, d=256 6430 GB/s on the Products graph.
+    if (d4 <= 8) return launch_mean<4, 8, 1, 4, 6>(a, s);
+    if (d4 <= 16) return launch_mean<4, 16, 1, 4, 6>(a, s);
+    if (d4 <= 32) return launch_mean<4, 32, 1, 4, 8>(a, s);
+    if (d4 <= 64) return launch_mean<4, 32, 2, 3, 5>(a, s);
     if (d4 <= 128) return launch_mean<4, 32, 4, 2>(a, s);
     return launch_mean<4, 32, 8, 2>(a, s);
   }
@@ -584,7 +597,8 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
                         const int32_t* indices, const int64_t* row_ids, int64_t row_base,
                         const int64_t* self_rows, const int32_t* col_map, const float* h,
                         int64_t ld_h, float* out, int64_t ld_out, const int32_t* schedule,
-                        int64_t n_hub, glint_stream_t stream) {
+                        int64_t n_hub, const float* bias, int32_t act,
+                        glint_stream_t stream) {
   GLINT_REQUIRE(n_rows >= 0, "spmm_mean: n_rows must be >= 0");
   if (n_rows == 0) return GLINT_OK;
   GLINT_REQUIRE(dim > 0, "spmm_mean: dim must be > 0");
@@ -592,6 +606,7 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
   GLINT_REQUIRE(ld_h >= dim && ld_out >= dim, "spmm_mean: leading dimension < dim");
   GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows, "spmm_mean: n_hub out of range");
   GLINT_REQUIRE(schedule || n_hub == 0, "spmm_mean: hub rows need a schedule");
+  GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "spmm_mean: bad act %d", act);
   MeanArgs a;
   a.ra = RowAddr{indptr, indices, row_ids, row_base, self_rows, col_map};
   a.dim = dim;
@@ -599,6 +614,8 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
   a.ld_h = ld_h;
   a.out = out;
   a.ld_out = ld_out;
+  a.bias = bias;
+  a.act = act;
   a.sc.schedule = schedule;
   a.sc.n_rows = n_rows;
   a.sc.n_hub = n_hub;

@@ -124,7 +124,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // one of hi / lo
   static constexpr int W_BYTES = BN * BK * 4;
   static constexpr int STAGE = 2 * A_BYTES + 2 * W_BYTES;
-  static constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;
+  static constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4 + 4 * BN * 4;  // staging + bias copies
   static constexpr int SMEM = STAGES * STAGE + EPI_BYTES;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -194,8 +194,8 @@ __device__ __forceinline__ uint32_t tile_off(int r, int c) {
 }
 
 template <int ACT>
-__device__ __forceinline__ float epilogue_op(float x, const float* bias, int col) {
-  if (bias) x = __fadd_rn(x, __ldg(bias + col));
+__device__ __forceinline__ float epilogue_op(float x, const float* bias_s, bool has_bias) {
+  if (has_bias) x = __fadd_rn(x, *bias_s);
   if (ACT == GLINT_ACT_RELU) x = (x > 0.0f || x != x) ? x : 0.0f;
   if (ACT == GLINT_ACT_LEAKY_RELU) x = x >= 0.0f ? x : __fmul_rn(0.2f, x);
   return x;
@@ -237,62 +237,83 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
 
   if (warp < kProducerWarps) {
     // ---------------------------------------------------------- producers
+    // Flattened (tile, k-block) steps of this CTA; group g takes steps
+    // g, g+2, ...  The loads of a group's next step are issued before it
+    // waits for a free stage and splits the current one (register double
+    // buffering), so two steps of global loads are in flight per thread.
     const int grp = warp >> 2;
     const int wq = warp & 3;
     const int rsub = lane & 7;
     const int chunk = lane >> 3;  // 0..3: 16-byte chunk within the BK=16 block
+    constexpr int WG = (BN / 8 + 3) / 4;
+    const int64_t my_tiles = blockIdx.x < a.num_tiles
+                                 ? (a.num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total = my_tiles * nkb;
     unsigned long long t_wait = 0, t_work = 0;
-    int64_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+
+    auto load_a = [&](int64_t idx, float4 (&va)[BM / 32]) {
+      const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
+      const int kb = static_cast<int>(idx % nkb);
       const int64_t m0 = (tile / a.n_tiles) * BM;
-      const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
-      for (int kb = grp; kb < nkb; kb += 2) {
-        const int64_t idx = it * nkb + kb;
-        const int s = static_cast<int>(idx % STAGES);
-        const uint32_t round = static_cast<uint32_t>(idx / STAGES);
-        const unsigned long long t0 = clock64();
-        mbar_wait(&empty_bar[s], (round & 1u) ^ 1u);
-        const unsigned long long t1 = clock64();
-        t_wait += t1 - t0;
-        uint8_t* a_hi = smem + s * C::STAGE;
-        uint8_t* a_lo = a_hi + C::A_BYTES;
-        uint8_t* w_hi = a_lo + C::A_BYTES;
-        uint8_t* w_lo = w_hi + C::W_BYTES;
-        const int k = kb * BK + 4 * chunk;
-        float4 va[BM / 32];
+      const int k = kb * BK + 4 * chunk;
 #pragma unroll
-        for (int i = 0; i < BM / 32; ++i) {
-          const int r = (wq + 4 * i) * 8 + rsub;  // 0..255
-          const int64_t row = m0 + r;
-          va[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < a.M)
-            va[i] = load4<VEC>(a.A + (a.a_rows ? a.a_rows[row] : row) * a.lda, k, a.K);
-        }
-        constexpr int WG = (BN / 8 + 3) / 4;
-        float4 vw[WG];
-#pragma unroll
-        for (int i = 0; i < WG; ++i) {
-          const int r = (wq + 4 * i) * 8 + rsub;
-          vw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (r < BN && n0 + r < a.N)
-            vw[i] = load4<VEC>(a.W + static_cast<int64_t>(n0 + r) * a.ldw, k, a.K);
-        }
-#pragma unroll
-        for (int i = 0; i < BM / 32; ++i) {
-          const int r = (wq + 4 * i) * 8 + rsub;
-          const uint32_t off = (r >= HALF ? C::A_BYTES / 2 : 0) + tile_off(r & (HALF - 1), chunk);
-          split_store(a_hi, a_lo, off, va[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < WG; ++i) {
-          const int r = (wq + 4 * i) * 8 + rsub;
-          if (r < BN) split_store(w_hi, w_lo, tile_off(r, chunk), vw[i]);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full_bar[s]);
-        t_work += clock64() - t1;
+      for (int i = 0; i < BM / 32; ++i) {
+        const int64_t row = m0 + (wq + 4 * i) * 8 + rsub;
+        va[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < a.M) va[i] = load4<VEC>(a.A + (a.a_rows ? a.a_rows[row] : row) * a.lda, k, a.K);
       }
+    };
+    auto store_step = [&](int64_t idx, const float4 (&va)[BM / 32]) {
+      // W (L2-resident) is loaded here, A was prefetched one step ahead.
+      const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
+      const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      const int k = static_cast<int>(idx % nkb) * BK + 4 * chunk;
+      float4 vw[WG];
+#pragma unroll
+      for (int i = 0; i < WG; ++i) {
+        const int r = (wq + 4 * i) * 8 + rsub;
+        vw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < BN && n0 + r < a.N)
+          vw[i] = load4<VEC>(a.W + static_cast<int64_t>(n0 + r) * a.ldw, k, a.K);
+      }
+      const int s = static_cast<int>(idx % STAGES);
+      const uint32_t round = static_cast<uint32_t>(idx / STAGES);
+      const unsigned long long t0 = clock64();
+      mbar_wait(&empty_bar[s], (round & 1u) ^ 1u);
+      const unsigned long long t1 = clock64();
+      t_wait += t1 - t0;
+      uint8_t* a_hi = smem + s * C::STAGE;
+      uint8_t* a_lo = a_hi + C::A_BYTES;
+      uint8_t* w_hi = a_lo + C::A_BYTES;
+      uint8_t* w_lo = w_hi + C::W_BYTES;
+#pragma unroll
+      for (int i = 0; i < BM / 32; ++i) {
+        const int r = (wq + 4 * i) * 8 + rsub;
+        const uint32_t off = (r >= HALF ? C::A_BYTES / 2 : 0) + tile_off(r & (HALF - 1), chunk);
+        split_store(a_hi, a_lo, off, va[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < WG; ++i) {
+        const int r = (wq + 4 * i) * 8 + rsub;
+        if (r < BN) split_store(w_hi, w_lo, tile_off(r, chunk), vw[i]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[s]);
+      t_work += clock64() - t1;
+    };
+
+    float4 va0[BM / 32], va1[BM / 32];
+    int64_t idx = grp;
+    if (idx < total) load_a(idx, va0);
+    while (idx < total) {
+      if (idx + 2 < total) load_a(idx + 2, va1);
+      store_step(idx, va0);
+      idx += 2;
+      if (idx >= total) break;
+      if (idx + 2 < total) load_a(idx + 2, va0);
+      store_step(idx, va1);
+      idx += 2;
     }
     if (lane == 0) {
       prof_add(a, 0, t_wait);
@@ -349,11 +370,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
     // ------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     float* stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE) + (warp - kEpiWarp0) * 32 * EPI_LD;
+    float* bias_s = reinterpret_cast<float*>(smem + STAGES * C::STAGE) + 4 * 32 * EPI_LD +
+                    (warp - kEpiWarp0) * BN;
+    const bool has_bias = a.bias != nullptr;
+    int bias_n0 = -1;
     unsigned long long t_wait = 0, t_work = 0;
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
       const int64_t m0 = (tile / a.n_tiles) * BM;
       const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      if (has_bias && n0 != bias_n0) {   // this warp's copy of bias[n0, n0+BN)
+        __syncwarp();
+        for (int i = lane; i < BN; i += 32) bias_s[i] = n0 + i < a.N ? __ldg(a.bias + n0 + i) : 0.f;
+        __syncwarp();
+        bias_n0 = n0;
+      }
       const unsigned long long t0 = clock64();
       mbar_wait(&tmem_full, static_cast<uint32_t>(it) & 1u);
       const unsigned long long t1 = clock64();
@@ -369,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = n0 + c0 + i;
-            v[i] = col < a.N ? epilogue_op<ACT>(v[i], a.bias, col) : 0.0f;
+            v[i] = col < a.N ? epilogue_op<ACT>(v[i], bias_s + c0 + i, has_bias) : 0.0f;
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i)

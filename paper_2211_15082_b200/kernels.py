@@ -37,8 +37,10 @@ ELEMENTWISE_KINDS = ("ReLU", "LeakyReLU", "Add", "Norm", "DropoutIdentity")
 # whole CTA instead of one warp (see csrc/aggregate.cu).
 HUB_MIN_DEGREE = 512
 
-# GEMM precision used by linear / attention projection.
-PRECISION = _lib.PREC_FP32
+# GEMM precision used by linear / attention projection: split-TF32 on the
+# tcgen05 tensor cores (~1e-6 rel-L2 vs fp64); PREC_FP32 selects the CUDA-core
+# fp32 FMA-chain kernel.
+PRECISION = _lib.PREC_3XTF32
 
 
 def _torch():
@@ -310,12 +312,12 @@ def trivial_batch_csc(targets) -> BatchCsc:
 
 
 def spmm_mean(out, h, indptr, indices, n_rows, row_ids=None, row_base=0, self_rows=None,
-              col_map=None, schedule=None, n_hub=0):
+              col_map=None, schedule=None, n_hub=0, bias=None, act=0):
     """Raw K1 launch on device tensors (see glint_spmm_mean_f32)."""
     dim = int(out.shape[1])
     _lib.call("glint_spmm_mean_f32", int(n_rows), dim, ptr(indptr), ptr(indices), ptr(row_ids),
               int(row_base), ptr(self_rows), ptr(col_map), ptr(h), ld(h), ptr(out), ld(out),
-              ptr(schedule), int(n_hub), stream_handle())
+              ptr(schedule), int(n_hub), ptr(bias), int(act), stream_handle())
     return out
 
 

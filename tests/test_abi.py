@@ -35,7 +35,7 @@ def test_argument_errors_map_to_value_error_without_gpu():
     # validation happens on the host before any CUDA call
     with pytest.raises(ValueError, match="n_rows"):
         _lib.call("glint_spmm_mean_f32", -1, 4, None, None, None, 0, None, None, None, 4, None, 4,
-                  None, 0, None)
+                  None, 0, None, 0, None)
     with pytest.raises(ValueError, match="unknown kind"):
         _lib.call("glint_elementwise_f32", 99, 1, 1, 1, None, None, None, None, 1, None)
     with pytest.raises(ValueError, match="heads"):

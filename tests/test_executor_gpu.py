@@ -85,6 +85,29 @@ def test_outputs_invariant_to_batching_and_order(golden, cuda):
                 assert out.tobytes() == base.tobytes(), (th, order)
 
 
+def test_reassociation_and_precision_agree(golden, cuda):
+    """Transform-then-aggregate (narrowing ConvMean) and both GEMM precisions
+    agree with the aggregate-first fp32 path within 1e-5 (bar 1e-4)."""
+    from paper_2211_15082_b200 import _lib
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.synth import build_gcn, build_jknet
+
+    arrs, _ = golden
+    g = golden_graph(arrs, "pow300")
+    x = arrs["e/pow300/x"]
+    for m in (build_gcn(8, 16, 4, 3, seed=11), build_jknet(8, 6, 4, 3, seed=12)):
+        want = orc.eval_model(orc.model_spec(m), g.indptr, g.indices, x)
+        base = run_inference(m, g, x, budget=DeviceBudget(1 << 30), reassociate=False,
+                             precision=_lib.PREC_FP32).output
+        for reassoc in (False, True):
+            for prec in (_lib.PREC_FP32, _lib.PREC_3XTF32):
+                out = run_inference(m, g, x, budget=DeviceBudget(1 << 30), reassociate=reassoc,
+                                    precision=prec).output
+                assert rel_l2(out, base) <= 1e-5, (reassoc, prec)
+                assert rel_l2(out, want) <= 1e-5, (reassoc, prec)
+
+
 def test_device_budget_and_device_output(golden, cuda):
     import torch
 

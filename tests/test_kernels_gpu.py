@@ -90,6 +90,28 @@ def test_agg_mean_widths_and_hubs_bit_exact(cuda, dim):
     assert not out[:, dim:].any()
 
 
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_agg_mean_bias_act_epilogue_bit_exact(cuda, act):
+    """K1 epilogue act(mean + b) == numpy (agg_mean + b) then ReLU/LeakyReLU, bytes."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels
+    from paper_2211_15082_b200.synth import gen_powerlaw
+
+    g = gen_powerlaw(700, seed=5)
+    rng = np.random.default_rng(act)
+    x = rng.normal(size=(700, 48)).astype(np.float32)
+    b = rng.normal(size=48).astype(np.float32)
+    want = orc.agg_mean(orc.build_batch_csc(g.indptr, g.indices, np.arange(700)), x) + b
+    want = [want, orc.elementwise("ReLU", [want]), orc.leaky_relu(want)][act]
+    dg = kernels.device_graph(g)
+    out = torch.empty((700, 48), device="cuda")
+    sched, nh = kernels.degree_schedule(dg.indptr, None, 0, 700)
+    kernels.spmm_mean(out, torch.from_numpy(x).cuda(), dg.indptr, dg.indices, 700,
+                      schedule=sched, n_hub=int(nh.item()), bias=torch.from_numpy(b).cuda(), act=act)
+    assert out.cpu().numpy().tobytes() == want.tobytes()
+
+
 def test_agg_mean_reference_kats(cuda):
     """Reference test_kernels.py:50-67 known answers."""
     from paper_2211_15082_b200 import kernels
