@@ -51,7 +51,9 @@ def test_all_golden_cases(golden, cuda):
 
 def test_nodewise_equals_layerwise_bytes(golden, cuda):
     """Both engines share kernels; batch invariance makes them bit-identical
-    (reference test_executor.py:109-180)."""
+    (reference test_executor.py:109-180).  Compared on the aggregate-first
+    path: the layer-wise reassociation of narrowing convs is a different (but
+    equally row-invariant) fp32 evaluation order."""
     from test_host_logic import golden_models
 
     arrs, meta = golden
@@ -60,7 +62,7 @@ def test_nodewise_equals_layerwise_bytes(golden, cuda):
     for case in meta["e2e"]:
         if case["graph"] not in ("toy", "reg200") or case["budget"] != 1 << 30:
             continue
-        lw = _run(case, arrs, models)
+        lw = _run(case, arrs, models, reassociate=False)
         nw = _run(case, arrs, models, executor="nodewise", batch_size=7)
         assert lw.output.tobytes() == nw.output.tobytes(), case["name"]
         done += 1

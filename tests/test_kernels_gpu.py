@@ -229,7 +229,7 @@ def test_linear_row_invariance(cuda):
     full = kernels.linear(x, w, b)
     for i in (0, 1, 150, 299):
         assert kernels.linear(x[i:i + 1], w, b).tobytes() == full[i:i + 1].tobytes()
-    assert rel_l2(full, orc.linear(x, w, b)) <= 1e-6
+    assert rel_l2(full, orc.linear(x, w, b)) <= 5e-6
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 47, 100), (300, 47, 100), (1000, 256, 256),
