@@ -213,6 +213,11 @@ size_t glint_scan_workspace_bytes(int64_t n);
 int glint_degree_prefix(const int64_t* indptr, const int64_t* targets,
                         int64_t base, int64_t n, int64_t* out, void* ws,
                         size_t ws_bytes, glint_stream_t stream);
+/* Exclusive prefix of hub flags [deg(t)+1 >= min_degp1] over the same target
+ * addressing (sizes the hub path of a batch without a host pass over N). */
+int glint_hub_prefix(const int64_t* indptr, const int64_t* targets, int64_t base,
+                     int64_t n, int64_t min_degp1, int64_t* out, void* ws,
+                     size_t ws_bytes, glint_stream_t stream);
 /* Concatenated in-neighbour slices (kernels.py:56-68 gather_slices):
  * srcs[local_indptr[j] + k] = indices[indptr[t_j] + k]; either output may
  * be NULL; local positions through an idset when pos_ws != NULL

@@ -63,6 +63,7 @@ SIGNATURES = {
     "glint_idset_rank_map": (ctypes.c_int, [_P, _I64, _P, _P]),
     "glint_scan_workspace_bytes": (_SZ, [_I64]),
     "glint_degree_prefix": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _SZ, _P]),
+    "glint_hub_prefix": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
     "glint_gather_slices": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _I64, _P,
                                            _P, _P]),
     "glint_relabel_csc": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P]),
@@ -102,7 +103,7 @@ def last_error() -> str:
 # Kernels launched per call (for the bench's launch count); host-only or
 # memset-only entry points launch none.
 KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
-                    "glint_degree_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
+                    "glint_degree_prefix": 3, "glint_hub_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
                     "glint_device_info": 0, "glint_set_tuning": 0, "glint_debug_counters": 0}
 LAUNCHES = [0]
 

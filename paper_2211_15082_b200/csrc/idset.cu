@@ -96,6 +96,17 @@ struct DegreeFn {
   }
 };
 
+struct HubFn {  // 1 when deg + 1 >= min_degp1
+  const int64_t* indptr;
+  const int64_t* targets;
+  int64_t base;
+  int64_t min_degp1;
+  __device__ __forceinline__ int64_t operator()(int64_t j) const {
+    const int64_t t = targets ? targets[j] : base + j;
+    return (indptr[t + 1] - indptr[t] + 1) >= min_degp1 ? 1 : 0;
+  }
+};
+
 struct PopcFn {
   const uint32_t* bm;
   __device__ __forceinline__ int64_t operator()(int64_t w) const { return __popc(bm[w]); }
@@ -386,6 +397,16 @@ int glint_degree_prefix(const int64_t* indptr, const int64_t* targets, int64_t b
                 "degree_prefix: workspace too small");
   return exclusive_scan(n, DegreeFn{indptr, targets, base}, out, static_cast<int64_t*>(ws),
                         as_stream(stream));
+}
+
+int glint_hub_prefix(const int64_t* indptr, const int64_t* targets, int64_t base, int64_t n,
+                     int64_t min_degp1, int64_t* out, void* ws, size_t ws_bytes,
+                     glint_stream_t stream) {
+  GLINT_REQUIRE(indptr && out && n >= 0 && min_degp1 >= 0, "hub_prefix: bad argument");
+  GLINT_REQUIRE(n == 0 || (ws && ws_bytes >= glint_scan_workspace_bytes(n)),
+                "hub_prefix: workspace too small");
+  return exclusive_scan(n, HubFn{indptr, targets, base, min_degp1}, out,
+                        static_cast<int64_t*>(ws), as_stream(stream));
 }
 
 int glint_gather_slices(const int64_t* indptr, const int32_t* indices, const int64_t* targets,

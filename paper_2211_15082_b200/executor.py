@@ -38,7 +38,7 @@ from .errors import ConfigError, DeviceCapacityError, InternalError
 from .model_ir import ModelGraph
 from .reorder import NodeOrder, apply_order_device, make_order
 from .splitter import INPUT_REF, BlockSchedule, TensorRef, split
-from .storage import CscGraph, DeviceGraph, DeviceStore, EmbeddingStore, pitch_of
+from .storage import CscGraph, DeviceGraph, DeviceStore, EmbeddingStore, arange_ids, pitch_of
 
 MODES = ("full", "partial", "sampling")
 
@@ -149,11 +149,11 @@ def annotate(g, targets, depth, mode, fanout=None, seed=0) -> TargetSets:
     if mode == "sampling":
         if fanout is None or fanout < 1:
             raise ConfigError("sampling mode requires fanout >= 1")
-        every = np.arange(n, dtype=np.int64)
+        every = arange_ids(n)
         sampled = {l: sample_neighbors(g, every, fanout, seed, l) for l in range(1, depth + 1)}
     if depth == 0:
         return TargetSets(mode, 0, {0: targets}, sampled)
-    every = np.arange(n, dtype=np.int64)
+    every = arange_ids(n)
     if mode == "full":
         return TargetSets(mode, depth, {l: every for l in range(1, depth + 1)}, sampled)
     v_sets = {depth: targets}
@@ -303,6 +303,7 @@ class _Plan:
     end: int
     num_inputs: int
     num_edges: int
+    num_hubs: int = 0
 
 
 class _Params:
@@ -364,15 +365,14 @@ class LayerwiseEngine:
             dg = self._graph_cache[layer] = DeviceGraph.from_host(gl, self.dev)
         return dg
 
-    def _hub_counter(self, gl: DeviceGraph, targets_np, full):
-        """Host prefix of hub rows (deg+1 >= HUB_MIN_DEGREE) over the layer's targets."""
-        key = ("hub", id(gl), None if full else id(targets_np))
+    def _hub_counter(self, gl: DeviceGraph, targets_dev, full):
+        """Device prefix of hub rows (deg+1 >= HUB_MIN_DEGREE) over the layer's targets."""
+        if not full:
+            return kernels.hub_prefix_dev(gl, targets_dev)
+        key = ("hubpre", kernels.HUB_MIN_DEGREE)
         pre = gl._cache.get(key)
         if pre is None:
-            deg = gl.in_degrees if full else gl.in_degrees[targets_np]
-            pre = np.zeros(len(deg) + 1, dtype=np.int64)
-            np.cumsum(deg + 1 >= kernels.HUB_MIN_DEGREE, out=pre[1:])
-            gl._cache[key] = pre
+            pre = gl._cache[key] = kernels.hub_prefix_dev(gl, None, 0, gl.num_nodes)
         return pre
 
     def _reassociate(self, o) -> bool:
@@ -404,7 +404,7 @@ class LayerwiseEngine:
 
     # -- planning -------------------------------------------------------------
 
-    def _planner(self, blk, gl, targets_dev, targets_np, full, prefix):
+    def _planner(self, blk, gl, targets_dev, targets_np, full, prefix, hub_pre):
         import torch
 
         n_nodes = gl.num_nodes
@@ -413,10 +413,16 @@ class LayerwiseEngine:
         def plan_fn(start, end):
             n_t = end - start
             n_e = int(prefix[end] - prefix[start]) if blk.has_conv else 0
+            n_h = 0
             if not blk.has_conv or n_t == 0:
                 n_i = n_t
             elif full and n_t == n_nodes:
                 n_i = n_t
+                key = ("hubtotal", kernels.HUB_MIN_DEGREE)
+                if key not in gl._cache:
+                    with torch.cuda.stream(self.plan_stream):
+                        gl._cache[key] = int(hub_pre[n_nodes].item())
+                n_h = gl._cache[key]
             else:
                 key = id(gl)
                 ids = self._plan_sets.get(key)
@@ -432,9 +438,11 @@ class LayerwiseEngine:
                         sl = targets_dev[start:end]
                         ids.add_ids(sl).add_neighbors(gl, sl)
                     ids.finalize()
-                    n_i = ids.count()
+                    counts = torch.stack([ids.count_dev[0],
+                                          hub_pre[end] - hub_pre[start]]).cpu()
+                    n_i, n_h = int(counts[0]), int(counts[1])
             fp = devmodel.footprint_counts(blk, n_t, n_i, n_e, dims)
-            return _Plan(start, end, n_i, n_e), fp
+            return _Plan(start, end, n_i, n_e, n_h), fp
 
         return plan_fn
 
@@ -546,7 +554,7 @@ class LayerwiseEngine:
                       _prefix_host(gl.in_degrees, targets_np))
         else:
             prefix = np.zeros(len(targets_np) + 1, dtype=np.int64)
-        hub_pre = self._hub_counter(gl, targets_np, full) if blk.has_conv else None
+        hub_pre = self._hub_counter(gl, targets_dev, full) if blk.has_conv else None
         layer_mats, layer_spaces = self._layer_inputs(blk, gl, targets_dev, full)
         fused = self._fusions(blk)
         gat_cache = {}
@@ -557,7 +565,7 @@ class LayerwiseEngine:
                             hub_pre, gat_cache)
 
         self.plan_stream.wait_stream(torch.cuda.current_stream(self.dev))
-        plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix)
+        plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix, hub_pre)
         sub_targets = targets_np[lo:hi] if (lo, hi) != (0, len(targets_np)) else targets_np
         sub_prefix = prefix[lo:hi + 1] - prefix[lo] if (lo, hi) != (0, len(targets_np)) else prefix
 
@@ -618,7 +626,7 @@ class LayerwiseEngine:
             return self.stores[key].view(), self.spaces[key].rank_map
 
         sched = self._schedule(gl, row_ids, row_base, B, full) if blk.has_conv else None
-        n_hub = int(hub_pre[e] - hub_pre[s]) if hub_pre is not None else 0
+        n_hub = plan.num_hubs
 
         skip = set(fused.values())
         for o in blk.op_ids:
@@ -1033,7 +1041,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     if executor not in ("layerwise", "nodewise"):
         raise ConfigError(f"unknown executor {executor!r}")
     if mode == "full" or targets is None:
-        user_targets = np.arange(g.num_nodes, dtype=np.int64)
+        user_targets = arange_ids(g.num_nodes)
     else:
         user_targets = np.asarray(targets, dtype=np.int64)
         if len(user_targets) != len(np.unique(user_targets)):
@@ -1069,7 +1077,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         if ex is not None:
             ex.exchange_tensor(store.data)      # every rank returns the full output
         row_ids = tsets.v_sets[m.depth if m.depth else 0]
-        out_dev = _gather_rows(store, row_ids, node_order.inv[user_targets], dg0.device)
+        wanted = user_targets if node_order.is_identity() else node_order.inv[user_targets]
+        out_dev = _gather_rows(store, row_ids, wanted, dg0.device)
     else:
         bud = resolve_budget(budget)
         out_sorted = infer_nodewise(m, g_i, x_i, internal, batch_size, bud, stats,
@@ -1106,8 +1115,10 @@ def _resident_bytes(m, schedule, tsets, g):
 
 
 def _is_arange(a) -> bool:
-    """a == arange(len(a)) (cheap checks first)."""
+    """a == arange(len(a)) (O(1) for the cached identity, cheap checks first)."""
     n = len(a)
+    if a is arange_ids(n):
+        return True
     return n == 0 or (a[0] == 0 and a[-1] == n - 1 and bool(np.all(np.diff(a) == 1)))
 
 

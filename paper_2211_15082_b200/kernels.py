@@ -208,6 +208,20 @@ def degree_prefix_dev(g, targets=None, base=0, n=0):
     return out
 
 
+def hub_prefix_dev(g, targets=None, base=0, n=0, hub_min=None):
+    """Device exclusive prefix of hub flags (deg+1 >= HUB_MIN_DEGREE) over targets."""
+    torch = _torch()
+    hub_min = HUB_MIN_DEGREE if hub_min is None else hub_min
+    if targets is not None:
+        n = targets.shape[0]
+    out = torch.empty(n + 1, dtype=torch.int64, device=g.indptr.device)
+    wsb = _lib.query("glint_scan_workspace_bytes", n)
+    ws = torch.empty((wsb + 7) // 8, dtype=torch.int64, device=g.indptr.device)
+    _lib.call("glint_hub_prefix", ptr(g.indptr), ptr(targets), int(base), int(n), int(hub_min),
+              ptr(out), ptr(ws), wsb, stream_handle())
+    return out
+
+
 def degree_schedule(indptr, row_ids=None, row_base=0, n_rows=0, hub_min=None):
     """Longest-first row order (int32) and hub count, computed on the device.
 

@@ -34,8 +34,14 @@ class NodeOrder:
     perm: np.ndarray
 
     def __post_init__(self):
+        from .storage import arange_ids
+
         perm = np.ascontiguousarray(self.perm, dtype=np.int64)
         n = len(perm)
+        if perm is arange_ids(n):          # cached identity: nothing to check or invert
+            object.__setattr__(self, "perm", perm)
+            object.__setattr__(self, "_inv", perm)
+            return
         if n and not (perm[0] == 0 and perm[-1] == n - 1 and np.all(np.diff(perm) == 1)):
             seen = np.zeros(n, dtype=bool)
             ok = perm.min() >= 0 and perm.max() < n
@@ -57,11 +63,17 @@ class NodeOrder:
         return len(self.perm)
 
     def is_identity(self) -> bool:
+        from .storage import arange_ids
+
+        if self.perm is arange_ids(self.num_nodes):
+            return True
         return bool(np.array_equal(self.perm, np.arange(self.num_nodes)))
 
 
 def identity_order(g) -> NodeOrder:
-    return NodeOrder(np.arange(g.num_nodes, dtype=np.int64))
+    from .storage import arange_ids
+
+    return NodeOrder(arange_ids(g.num_nodes))
 
 
 def _host_csc(g):

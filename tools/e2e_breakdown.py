@@ -69,6 +69,15 @@ def main():
         out["run_inference_ms"] = (time.perf_counter() - t0) * 1e3
         del res, dg, x, store, eng
     print(json.dumps(out), flush=True)
+    import cProfile
+    import pstats
+
+    pr = cProfile.Profile()
+    pr.enable()
+    res = run_inference(m, hg, xh, budget=budget, output="numpy")
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
 
 
 if __name__ == "__main__":
