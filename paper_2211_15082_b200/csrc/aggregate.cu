@@ -21,6 +21,8 @@
 //     in descending degree-bucket order.
 #include <cub/block/block_reduce.cuh>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace glint {
@@ -230,6 +232,152 @@ __global__ void __launch_bounds__(kThreads, MINB) mean_kernel(MeanArgs a) {
   mean_row_regular<VEC, LPR, VPL, U>(a, r, lane_g, gmask);
 }
 
+// ------------------------------------------------- hub rows: bulk-copy ring --
+//
+// One CTA per (hub row, 256-column slice).  Warps 0-7 are consumers, one
+// column per thread, adding source rows in stored edge order from a shared
+// ring; warp 8 is the producer: it streams whole source-row slices into the
+// ring with cp.async.bulk (the TMA engine, completion counted on an mbarrier
+// per group of slots).  ~96 KB of row data stay in flight per CTA, so a
+// 20K-neighbour hub row is bandwidth- rather than latency-bound, while each
+// column keeps its single sequential add chain (bit-exact).
+constexpr int kHubRingBytes = 96 * 1024;
+constexpr int kHubGroups = 8;               // ring = 8 groups of slots
+constexpr int kHubThreads = 9 * 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void hub_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n"
+      :
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int slots_per_group,
+                                                               int slice_floats) {
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full_bar[kHubGroups];
+  __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
+  const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
+  const int64_t r = a.sc.schedule[blockIdx.x / a.sc.hub_col_blocks];
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int c0 = cb * slice_floats;
+  const int width = min(slice_floats, a.dim - c0);
+  const uint32_t slice_bytes = static_cast<uint32_t>(((width + 3) / 4) * 16);
+  const int64_t deg = end - beg;
+  const int64_t ngroups = (deg + slots_per_group - 1) / slots_per_group;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < kHubGroups; ++g) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[g])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&empty_bar[g])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // producer: group gi -> ring group gi % kHubGroups
+    for (int64_t gi = 0; gi < ngroups; ++gi) {
+      const int g = static_cast<int>(gi % kHubGroups);
+      const uint32_t round = static_cast<uint32_t>(gi / kHubGroups);
+      if (round > 0) hub_mbar_wait(&empty_bar[g], (round - 1) & 1u);
+      const int64_t e0 = beg + gi * slots_per_group;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(smem_u32(&full_bar[g])), "r"(slice_bytes * cnt) : "memory");
+      }
+      __syncwarp();
+      float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
+      for (int j = lane; j < cnt; j += 32) {
+        const int64_t u = a.ra.map(a.ra.indices[e0 + j]);
+        const float* src = a.h + u * a.ld_h + c0;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_u32(slot0 + static_cast<int64_t>(j) * slice_floats)), "l"(src),
+            "r"(slice_bytes), "r"(smem_u32(&full_bar[g]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  // consumers: thread t owns column c0 + t
+  const int col = c0 + threadIdx.x;
+  const bool active = threadIdx.x < width;
+  float acc = 0.0f;
+  for (int64_t gi = 0; gi < ngroups; ++gi) {
+    const int g = static_cast<int>(gi % kHubGroups);
+    const uint32_t round = static_cast<uint32_t>(gi / kHubGroups);
+    hub_mbar_wait(&full_bar[g], round & 1u);
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group),
+                                         end - (beg + gi * slots_per_group)));
+    const float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
+    if (active) {
+      for (int j = 0; j < cnt; ++j) acc = __fadd_rn(acc, slot0[j * slice_floats + threadIdx.x]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
+                                ::"r"(smem_u32(&empty_bar[g])) : "memory");
+  }
+  if (active) {
+    const int64_t self_off = a.ra.self_row(r, rid) * a.ld_h;
+    acc = __fadd_rn(acc, __ldg(a.h + self_off + col));
+    const float degp1 = static_cast<float>(deg + 1);
+    a.out[r * a.ld_out + col] = mean_epilogue(a, __fdiv_rn(acc, degp1), col);
+  }
+}
+
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+// Library-internal side stream (per device) for the concurrent hub kernel.
+int side_stream(SideStream** out) {
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  GLINT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.stream) {
+    GLINT_CUDA(cudaStreamCreateWithFlags(&ss.stream, cudaStreamNonBlocking));
+    GLINT_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    GLINT_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return GLINT_OK;
+}
+
+int launch_hub(const MeanArgs& a, cudaStream_t s) {
+  // slice of <= 256 columns per CTA, whole slice per bulk copy
+  const int slice = 256;
+  const int width = std::min(slice, a.dim);
+  const int slice_floats = ((width + 3) / 4) * 4;
+  int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
+  per_group = std::max(1, std::min(per_group, 64));
+  const int smem = per_group * kHubGroups * slice_floats * 4;
+  static bool configured = false;
+  if (!configured) {
+    GLINT_CUDA(cudaFuncSetAttribute(mean_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kHubRingBytes + 4096));
+    configured = true;
+  }
+  mean_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kHubThreads, smem, s>>>(a, per_group,
+                                                                                 slice_floats);
+  return launch_status("spmm_mean_hub");
+}
+
 template <int VEC, int LPR, int VPL, int U, int MINB = 3>
 int launch_mean(const MeanArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
@@ -244,7 +392,31 @@ int launch_mean(const MeanArgs& a, cudaStream_t s) {
   return launch_status("spmm_mean");
 }
 
+int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s);
+
+// Hub rows go to the bulk-copy kernel on a side stream (fork/join with
+// events, so the caller's stream order is preserved and graph capture works);
+// the regular kernel runs concurrently on the caller's stream.
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
+  if (!vec4 || a.sc.hub_ctas == 0 || tuning(GLINT_TUNE_HUB_INLINE))
+    return dispatch_regular(a, vec4, s);
+  SideStream* ss = nullptr;
+  int rc = side_stream(&ss);
+  if (rc) return rc;
+  GLINT_CUDA(cudaEventRecord(ss->fork, s));
+  GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
+  rc = launch_hub(a, ss->stream);
+  if (rc) return rc;
+  GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
+  MeanArgs reg = a;
+  reg.sc.hub_ctas = 0;  // hub schedule entries are skipped, not processed
+  rc = dispatch_regular(reg, vec4, s);
+  if (rc) return rc;
+  GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+  return GLINT_OK;
+}
+
+int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
   // Tuning variants (glint_set_tuning(GLINT_TUNE_MEAN_VARIANT, v)) for the
   // widths of the headline workload; 0 is the default.
   // Measured on B200 (tools/sweep_kernels.py, profiles/): 4 CTAs/SM (<= 64

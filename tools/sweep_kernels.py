@@ -79,6 +79,35 @@ def main():
                 same = bool(torch.equal(ref, out))
             print(json.dumps({"kernel": "spmm_mean", "dim": d, "variant": variant, "ms": ms,
                               "GBps": nb / ms / 1e6, "identical_to_v0": same}), flush=True)
+        # hub rows in the register path of the main kernel (vs bulk-copy hub kernel)
+        _lib.call("glint_set_tuning", 0, 0)
+        _lib.call("glint_set_tuning", 2, 1)
+        ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n, schedule=sched,
+                                             n_hub=hub_pre), args.reps)
+        _lib.call("glint_set_tuning", 2, 0)
+        print(json.dumps({"kernel": "spmm_mean_hub_inline", "dim": d, "ms": ms,
+                          "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
+                          "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+        # the bootstrap batch sizes of layer 1 (contiguous row ranges)
+        pos = 0
+        for size in (1024, 4096, 16384, 65536, 262144, 1048576):
+            if pos + size > n:
+                break
+            hp = kernels.hub_prefix_dev(g, None, pos, size)
+            nh_r = int(hp[-1].item())
+            sch, _ = kernels.degree_schedule(g.indptr, None, pos, size)
+            o2 = out[pos:pos + size]
+            for inline in (0, 1):
+                _lib.call("glint_set_tuning", 2, inline)
+                ms = timed(lambda: kernels.spmm_mean(o2, h, g.indptr, g.indices, size,
+                                                     row_base=pos, schedule=sch, n_hub=nh_r),
+                           args.reps)
+                e_r = int(g.indptr_host[pos + size] - g.indptr_host[pos])
+                print(json.dumps({"kernel": "spmm_mean_batch", "dim": d, "rows": size,
+                                  "hubs": nh_r, "hub_inline": inline, "ms": ms,
+                                  "GBps": agg_bytes(d, e_r, size) / ms / 1e6}), flush=True)
+            _lib.call("glint_set_tuning", 2, 0)
+            pos += size
         # natural order, no hub path (effect of the LPT schedule)
         _lib.call("glint_set_tuning", 0, 0)
         ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n))
