@@ -286,28 +286,46 @@ __global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int s
   __syncthreads();
 
   if (warp == 8) {
-    // producer: group gi -> ring group gi % kHubGroups
-    for (int64_t gi = 0; gi < ngroups; ++gi) {
-      const int g = static_cast<int>(gi % kHubGroups);
-      const uint32_t round = static_cast<uint32_t>(gi / kHubGroups);
-      if (round > 0) hub_mbar_wait(&empty_bar[g], (round - 1) & 1u);
-      const int64_t e0 = beg + gi * slots_per_group;
-      const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                     ::"r"(smem_u32(&full_bar[g])), "r"(slice_bytes * cnt) : "memory");
+    // producer: group gi -> ring group gi % kHubGroups; lane j owns slot j
+    // (slots_per_group <= 32).  The source ids of a whole ring cycle (8
+    // groups) are loaded one cycle ahead, so no dependent index load sits
+    // between two groups' copies.
+    const int64_t ncycles = (ngroups + kHubGroups - 1) / kHubGroups;
+    auto load_cycle = [&](int64_t c, int64_t (&ids)[kHubGroups]) {
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) {
+        const int64_t e = beg + (c * kHubGroups + t) * slots_per_group + lane;
+        ids[t] = (lane < slots_per_group && e < end) ? a.ra.map(a.ra.indices[e]) : 0;
       }
-      __syncwarp();
-      float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
-      for (int j = lane; j < cnt; j += 32) {
-        const int64_t u = a.ra.map(a.ra.indices[e0 + j]);
-        const float* src = a.h + u * a.ld_h + c0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_u32(slot0 + static_cast<int64_t>(j) * slice_floats)), "l"(src),
-            "r"(slice_bytes), "r"(smem_u32(&full_bar[g]))
-            : "memory");
+    };
+    int64_t cur[kHubGroups], nxt[kHubGroups];
+    if (ncycles > 0) load_cycle(0, cur);
+    for (int64_t c = 0; c < ncycles; ++c) {
+      if (c + 1 < ncycles) load_cycle(c + 1, nxt);
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) {
+        const int64_t gi = c * kHubGroups + t;
+        if (gi < ngroups) {
+          if (c > 0) hub_mbar_wait(&empty_bar[t], static_cast<uint32_t>(c - 1) & 1u);
+          const int64_t e0 = beg + gi * slots_per_group;
+          const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
+          if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(smem_u32(&full_bar[t])), "r"(slice_bytes * cnt) : "memory");
+          }
+          __syncwarp();
+          if (lane < cnt) {
+            float* dst = ring + (static_cast<int64_t>(t) * slots_per_group + lane) * slice_floats;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                ::"r"(smem_u32(dst)), "l"(a.h + cur[t] * a.ld_h + c0), "r"(slice_bytes),
+                "r"(smem_u32(&full_bar[t]))
+                : "memory");
+          }
+        }
       }
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) cur[t] = nxt[t];
     }
     return;
   }
@@ -365,7 +383,7 @@ int launch_hub(const MeanArgs& a, cudaStream_t s) {
   const int width = std::min(slice, a.dim);
   const int slice_floats = ((width + 3) / 4) * 4;
   int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
-  per_group = std::max(1, std::min(per_group, 64));
+  per_group = std::max(1, std::min(per_group, 32));  // one producer lane per slot
   const int smem = per_group * kHubGroups * slice_floats * 4;
   static bool configured = false;
   if (!configured) {
