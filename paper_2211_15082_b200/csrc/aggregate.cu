@@ -14,11 +14,13 @@
 //     owns VPL 128-bit column chunks; U neighbour rows are loaded ahead of the
 //     adds (memory-level parallelism ~ U*VPL*16 B per lane).
 //   * hub rows (deg+1 >= hub_min, first n_hub entries of the degree-bucketed
-//     schedule): a whole 256-thread CTA owns (row, 256-column block); each
-//     thread owns one column and keeps UH loads in flight, source offsets are
-//     staged in shared memory.  Hub CTAs have the lowest blockIdx so they are
-//     dispatched first (longest-processing-time-first), regular rows follow
-//     in descending degree-bucket order.
+//     schedule): mean_hub_kernel on a side stream, one CTA per (row,
+//     64-column slice): a producer warp streams source-row slices into a
+//     64 KB shared ring with cp.async.bulk (TMA), one consumer thread per
+//     column adds them in stored order.  (Fallback for unaligned layouts: a
+//     256-thread CTA per (row, 256 columns) inside mean_kernel with register
+//     prefetch.)  Regular rows follow the hubs in descending degree-bucket
+//     order (longest-processing-time-first).
 #include <cub/block/block_reduce.cuh>
 
 #include <mutex>
@@ -241,9 +243,11 @@ __global__ void __launch_bounds__(kThreads, MINB) mean_kernel(MeanArgs a) {
 // per group of slots).  ~96 KB of row data stay in flight per CTA, so a
 // 20K-neighbour hub row is bandwidth- rather than latency-bound, while each
 // column keeps its single sequential add chain (bit-exact).
-constexpr int kHubRingBytes = 96 * 1024;
-constexpr int kHubGroups = 8;               // ring = 8 groups of slots
-constexpr int kHubThreads = 9 * 32;
+constexpr int kHubRingBytes = 64 * 1024;
+constexpr int kHubGroups = 8;               // ring = 8 groups of 32 slots
+constexpr int kHubSlice = 64;               // columns per hub CTA
+constexpr int kHubConsumerWarps = kHubSlice / 32;
+constexpr int kHubThreads = (kHubConsumerWarps + 1) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -260,12 +264,12 @@ __device__ __forceinline__ void hub_mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int slots_per_group,
-                                                               int slice_floats) {
+                                                               int slice_floats, int col_blocks) {
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full_bar[kHubGroups];
   __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
-  const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
-  const int64_t r = a.sc.schedule[blockIdx.x / a.sc.hub_col_blocks];
+  const int cb = static_cast<int>(blockIdx.x % col_blocks);
+  const int64_t r = a.sc.schedule[blockIdx.x / col_blocks];
   const int64_t rid = a.ra.csr_row(r);
   const int64_t beg = a.ra.indptr[rid];
   const int64_t end = a.ra.indptr[rid + 1];
@@ -279,13 +283,14 @@ __global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int s
   if (threadIdx.x == 0) {
     for (int g = 0; g < kHubGroups; ++g) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[g])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&empty_bar[g])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                   ::"r"(smem_u32(&empty_bar[g])), "r"(kHubConsumerWarps));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == 8) {
+  if (warp == kHubConsumerWarps) {
     // producer: group gi -> ring group gi % kHubGroups; lane j owns slot j
     // (slots_per_group <= 32).  The source ids of a whole ring cycle (8
     // groups) are loaded one cycle ahead, so no dependent index load sits
@@ -378,10 +383,11 @@ int side_stream(SideStream** out) {
 }
 
 int launch_hub(const MeanArgs& a, cudaStream_t s) {
-  // slice of <= 256 columns per CTA, whole slice per bulk copy
-  const int slice = 256;
-  const int width = std::min(slice, a.dim);
+  // slices of <= kHubSlice columns per CTA (several CTAs per hub row keep
+  // more bytes in flight per row), one bulk copy per source-row slice
+  const int width = std::min(kHubSlice, a.dim);
   const int slice_floats = ((width + 3) / 4) * 4;
+  const int col_blocks = static_cast<int>(ceil_div(a.dim, kHubSlice));
   int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
   per_group = std::max(1, std::min(per_group, 32));  // one producer lane per slot
   const int smem = per_group * kHubGroups * slice_floats * 4;
@@ -391,8 +397,9 @@ int launch_hub(const MeanArgs& a, cudaStream_t s) {
                                     kHubRingBytes + 4096));
     configured = true;
   }
-  mean_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kHubThreads, smem, s>>>(a, per_group,
-                                                                                 slice_floats);
+  const int64_t grid = a.sc.n_hub * col_blocks;
+  mean_hub_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(a, per_group, slice_floats,
+                                                                         col_blocks);
   return launch_status("spmm_mean_hub");
 }
 
