@@ -423,8 +423,13 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s);
 // events, so the caller's stream order is preserved and graph capture works);
 // the regular kernel runs concurrently on the caller's stream.
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
-  if (!vec4 || a.sc.hub_ctas == 0 || tuning(GLINT_TUNE_HUB_INLINE))
-    return dispatch_regular(a, vec4, s);
+  // The bulk-copy hub kernel wins when one hub row bounds the launch (small
+  // batches, measured up to ~10x); on large launches the register hub path
+  // inside the main kernel finishes within the regular rows' time and leaves
+  // shared memory to them (profiles/r01_spmm_sweep*.jsonl).
+  const int inline_knob = tuning(GLINT_TUNE_HUB_INLINE);  // 0 auto, 1 inline, 2 bulk
+  const bool use_bulk = inline_knob == 2 || (inline_knob == 0 && a.sc.n_rows < (1 << 19));
+  if (!vec4 || a.sc.hub_ctas == 0 || !use_bulk) return dispatch_regular(a, vec4, s);
   SideStream* ss = nullptr;
   int rc = side_stream(&ss);
   if (rc) return rc;

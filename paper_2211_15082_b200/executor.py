@@ -353,6 +353,8 @@ class LayerwiseEngine:
         self._sched_cache = {}
         self.kernel_launches = 0
         self.probe = None               # optional KernelProbe (bench roofline timing)
+        self.sink = None                # optional sink(store, row_lo, row_hi) for final rows
+        self.sink_chunks = 4
 
     # -- helpers ------------------------------------------------------------
 
@@ -560,9 +562,30 @@ class LayerwiseEngine:
         gat_cache = {}
         n_convs = sum(1 for _, k, _ in blk.iter_ops() if k in ("ConvMean", "ConvAttn"))
 
+        out_key = self.schedule.model_output.key
+        sink_store = (self.stores.get(out_key) if self.sink is not None
+                      and blk.block_id == self.schedule.model_output.block else None)
+
         def execute(plan: _Plan):
-            self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
-                            hub_pre, gat_cache)
+            if sink_store is None or plan.end - plan.start < 2 * self.sink_chunks:
+                self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
+                                hub_pre, gat_cache)
+                if sink_store is not None:
+                    self.sink(sink_store, plan.start, plan.end)
+                return
+            # Final block: run the batch as row chunks (row-invariant kernels, so
+            # identical bytes) and hand each finished chunk to the sink, which
+            # overlaps its device->host copy with the next chunk's kernels.
+            cuts = np.linspace(plan.start, plan.end, self.sink_chunks + 1).astype(np.int64)
+            hubs = (hub_pre[torch.from_numpy(cuts).to(self.dev)].cpu().numpy()
+                    if hub_pre is not None else np.zeros_like(cuts))
+            for k in range(self.sink_chunks):
+                lo, hi = int(cuts[k]), int(cuts[k + 1])
+                sub = _Plan(lo, hi, plan.num_inputs, int(prefix[hi] - prefix[lo]),
+                            int(hubs[k + 1] - hubs[k]))
+                self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
+                                hub_pre, gat_cache)
+                self.sink(sink_store, lo, hi)
 
         self.plan_stream.wait_stream(torch.cuda.current_stream(self.dev))
         plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix, hub_pre)
@@ -992,6 +1015,30 @@ def resolve_budget(budget, resident_bytes=0):
     return budget
 
 
+class _HostSink:
+    """Streams finished output rows to pinned host memory on a copy stream."""
+
+    def __init__(self, n_rows, dim, device):
+        import torch
+
+        self.host = torch.empty((n_rows, dim), dtype=torch.float32, pin_memory=True)
+        self.stream = torch.cuda.Stream(device=device)
+        self.device = device
+
+    def __call__(self, store, lo, hi):
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(ev)
+            self.host[lo:hi].copy_(store.view()[lo:hi], non_blocking=True)
+
+    def finish(self):
+        self.stream.synchronize()
+        return self.host.numpy()
+
+
 def _exchange_for(distributed, mode, g):
     """RowExchange when running full-mode inference across torch.distributed ranks."""
     if distributed is False or mode != "full":
@@ -1073,19 +1120,27 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         ex = _exchange_for(distributed, mode, g_i)
         eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision,
                               row_range=ex.row_range if ex else None, reassociate=reassociate)
+        row_ids = tsets.v_sets[m.depth if m.depth else 0]
+        streamed = None
+        if (host_out and ex is None and node_order.is_identity() and _is_arange(row_ids)
+                and len(row_ids) == g.num_nodes and user_targets is arange_ids(g.num_nodes)):
+            streamed = _HostSink(g.num_nodes, m.output_dim, dg0.device)
+            eng.sink = streamed
         store = eng.run(exchange=ex)
         if ex is not None:
             ex.exchange_tensor(store.data)      # every rank returns the full output
-        row_ids = tsets.v_sets[m.depth if m.depth else 0]
-        wanted = user_targets if node_order.is_identity() else node_order.inv[user_targets]
-        out_dev = _gather_rows(store, row_ids, wanted, dg0.device)
+        if streamed is None:
+            wanted = user_targets if node_order.is_identity() else node_order.inv[user_targets]
+            out_dev = _gather_rows(store, row_ids, wanted, dg0.device)
     else:
         bud = resolve_budget(budget)
         out_sorted = infer_nodewise(m, g_i, x_i, internal, batch_size, bud, stats,
                                     sampled=tsets.sampled, precision=precision)
         row_ids = internal
         out_dev = _gather_dense(out_sorted, row_ids, node_order.inv[user_targets])
-    if host_out:
+    if executor == "layerwise" and streamed is not None:
+        output_val = streamed.finish()
+    elif host_out:
         staging = torch.empty(tuple(out_dev.shape), dtype=torch.float32, pin_memory=True)
         staging.copy_(out_dev)
         output_val = staging.numpy()

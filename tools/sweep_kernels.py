@@ -97,7 +97,7 @@ def main():
             nh_r = int(hp[-1].item())
             sch, _ = kernels.degree_schedule(g.indptr, None, pos, size)
             o2 = out[pos:pos + size]
-            for inline in (0, 1):
+            for inline in (2, 1):      # 2 = bulk-copy hub kernel, 1 = register path
                 _lib.call("glint_set_tuning", 2, inline)
                 ms = timed(lambda: kernels.spmm_mean(o2, h, g.indptr, g.indices, size,
                                                      row_base=pos, schedule=sch, n_hub=nh_r),
