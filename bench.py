@@ -57,6 +57,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=None, help="target nodes per layer")
+    p.add_argument("--tune", action="append", default=[],
+                   help="diagnostics: glint_set_tuning KEY=VALUE (performance knobs only)")
+    p.add_argument("--timeline", action="store_true",
+                   help="diagnostics: add per-batch GPU timeline of the last timed step")
     return p.parse_args()
 
 
@@ -292,6 +296,9 @@ def main():
     _lib.load()
     if args.precision:
         kernels.PRECISION = _lib.PREC_3XTF32 if args.precision == "3xtf32" else _lib.PREC_FP32
+    for kv in args.tune:
+        k, v = kv.split("=")
+        _lib.call("glint_set_tuning", int(k), int(v))
     dev = torch.device("cuda", local)
     n, und, m, desc = workload(args)
     g, xt = make_graph_and_features(n, und, m.input_dim)
@@ -365,6 +372,9 @@ def main():
         "batches_per_step": st.batches,
         "layer_batches": st.layer_batches,
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks.report(),
+        **({"tuning": args.tune} if args.tune else {}),
+        **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()[-24:]]}
+           if args.timeline else {}),
     }
     line["config"]["capacity_bytes"] = budget.capacity
     line["config"]["gemm_precision"] = "3xtf32" if kernels.PRECISION == _lib.PREC_3XTF32 else "fp32"

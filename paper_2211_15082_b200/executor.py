@@ -567,6 +567,8 @@ class LayerwiseEngine:
                       and blk.block_id == self.schedule.model_output.block else None)
 
         def execute(plan: _Plan):
+            if self.probe is not None:
+                self.probe.mark(f"L{layer} plan->exec [{plan.start},{plan.end})")
             if sink_store is None or plan.end - plan.start < 2 * self.sink_chunks:
                 self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
                                 hub_pre, gat_cache)
@@ -779,8 +781,12 @@ class LayerwiseEngine:
                     st.release()
 
     def run(self, exchange=None):
+        if self.probe is not None:
+            self.probe.mark("start")
         for blk in self.schedule.blocks:
             self.run_block(blk)
+            if self.probe is not None:
+                self.probe.mark(f"L{blk.layer} last batch done")
             if exchange is not None:
                 exchange(self, blk)
             self.release_after(blk)
@@ -802,6 +808,7 @@ class KernelProbe:
 
     def __init__(self):
         self.records = []
+        self.marks = []
         self._open = None
 
     def begin(self, name):
@@ -819,6 +826,21 @@ class KernelProbe:
         name, start = self._open
         self.records.append((name, nbytes, start, ev))
         self._open = None
+
+    def mark(self, name):
+        """Timeline marker on the current stream (batch / layer boundaries)."""
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def timeline(self):
+        """[(name, ms since previous marker)] (call after synchronize)."""
+        out = []
+        for (_, e0), (name, e1) in zip(self.marks, self.marks[1:]):
+            out.append((name, e0.elapsed_time(e1)))
+        return out
 
     def summary(self):
         """{name: (launches, total bytes, total ms)} (call after synchronize)."""
