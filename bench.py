@@ -333,11 +333,17 @@ def main():
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record()
+        step_events = []
         for _ in range(args.steps):
             step(probe)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            step_events.append(ev)
         t_end.record()
         torch.cuda.synchronize()
         barrier(world)
+    step_ms = [t_start.elapsed_time(step_events[0])] + [
+        a.elapsed_time(b) for a, b in zip(step_events, step_events[1:])]
     launches = (_lib.LAUNCHES[0] - launches0) // max(args.steps, 1)
     ms = t_start.elapsed_time(t_end) / args.steps
     ms = max_over_ranks(ms, world)
@@ -372,6 +378,7 @@ def main():
         "batches_per_step": st.batches,
         "layer_batches": st.layer_batches,
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks.report(),
+        "step_ms": [round(t, 3) for t in step_ms],
         **({"tuning": args.tune} if args.tune else {}),
         **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()[-24:]]}
            if args.timeline else {}),
