@@ -380,7 +380,7 @@ def main():
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks.report(),
         "step_ms": [round(t, 3) for t in step_ms],
         **({"tuning": args.tune} if args.tune else {}),
-        **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()[-24:]]}
+        **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()]}
            if args.timeline else {}),
     }
     line["config"]["capacity_bytes"] = budget.capacity

@@ -306,8 +306,38 @@ class _Plan:
     num_hubs: int = 0
 
 
+_PLAN_STREAMS: dict = {}
+_PARAM_CACHE: dict = {}
+
+
+def _plan_stream(device):
+    """One planning side stream per device, reused by every engine."""
+    import torch
+
+    s = _PLAN_STREAMS.get(device)
+    if s is None:
+        s = _PLAN_STREAMS[device] = torch.cuda.Stream(device=device)
+    return s
+
+
+def _device_params(m: ModelGraph, device):
+    """Device weights of a model, uploaded once per (model, device) and kept
+    while the model object is alive (the model is immutable)."""
+    import weakref
+
+    key = (id(m), str(device))
+    hit = _PARAM_CACHE.get(key)
+    if hit is not None and hit[0]() is m:
+        return hit[1]
+    p = _Params(m, device)
+    for k in [k for k, (ref, _) in _PARAM_CACHE.items() if ref() is None]:
+        del _PARAM_CACHE[k]
+    _PARAM_CACHE[key] = (weakref.ref(m), p)
+    return p
+
+
 class _Params:
-    """Per-run device copies of model parameters (uploaded once)."""
+    """Device copies of model parameters."""
 
     def __init__(self, m: ModelGraph, device):
         import torch
@@ -341,11 +371,11 @@ class LayerwiseEngine:
         self.controller = BatchController(thresholds=thresholds, budget=budget)
         self.dev = g.indptr.device
         self.precision = kernels.PRECISION if precision is None else precision
-        self.params = _Params(m, self.dev)
+        self.params = _device_params(m, self.dev)
         self.dims = _dims_table(m, schedule)
         self.stores = {INPUT_REF: x}
         self.spaces = {INPUT_REF: _RowSpace()}
-        self.plan_stream = torch.cuda.Stream(device=self.dev)
+        self.plan_stream = _plan_stream(self.dev)
         self.users = m.consumers()
         self.row_range = row_range          # (lo, hi) node range owned by this rank (full mode)
         self._graph_cache = {}
@@ -426,11 +456,10 @@ class LayerwiseEngine:
                         gl._cache[key] = int(hub_pre[n_nodes].item())
                 n_h = gl._cache[key]
             else:
-                key = id(gl)
-                ids = self._plan_sets.get(key)
+                ids = gl._cache.get("plan_idset")      # reused across batches and runs
                 with torch.cuda.stream(self.plan_stream):
                     if ids is None:
-                        ids = self._plan_sets[key] = kernels.IdSet(n_nodes, self.dev)
+                        ids = gl._cache["plan_idset"] = kernels.IdSet(n_nodes, self.dev)
                     else:
                         _lib.call("glint_idset_clear", kernels.ptr(ids.ws), ids.n,
                                   kernels.stream_handle())
