@@ -122,6 +122,7 @@ def _expand_dev(dg, nodes_np):
     """sorted unique(nodes u in-neighbours(nodes)) via device id sets."""
     import torch
 
+    dg.wait_rows()
     ids = kernels.IdSet(dg.num_nodes, dg.indptr.device)
     if len(nodes_np):
         t = torch.from_numpy(np.ascontiguousarray(nodes_np, dtype=np.int64)).to(dg.indptr.device)
@@ -398,14 +399,21 @@ class LayerwiseEngine:
         return dg
 
     def _hub_counter(self, gl: DeviceGraph, targets_dev, full):
-        """Device prefix of hub rows (deg+1 >= HUB_MIN_DEGREE) over the layer's targets."""
+        """Prefix of hub rows (deg+1 >= HUB_MIN_DEGREE) over the layer's targets:
+        (device tensor, host copy or None).  Computed on the planning stream
+        (it needs only indptr, not the features or the edge ids)."""
+        import torch
+
         if not full:
-            return kernels.hub_prefix_dev(gl, targets_dev)
+            return kernels.hub_prefix_dev(gl, targets_dev), None
         key = ("hubpre", kernels.HUB_MIN_DEGREE)
-        pre = gl._cache.get(key)
-        if pre is None:
-            pre = gl._cache[key] = kernels.hub_prefix_dev(gl, None, 0, gl.num_nodes)
-        return pre
+        hit = gl._cache.get(key)
+        if hit is None:
+            self.plan_stream.wait_event(gl.indptr_event)
+            with torch.cuda.stream(self.plan_stream):
+                pre = kernels.hub_prefix_dev(gl, None, 0, gl.num_nodes)
+                hit = gl._cache[key] = (pre, pre.cpu().numpy())
+        return hit
 
     def _reassociate(self, o) -> bool:
         """Transform-then-aggregate for a ConvMean that narrows the row width.
@@ -436,7 +444,7 @@ class LayerwiseEngine:
 
     # -- planning -------------------------------------------------------------
 
-    def _planner(self, blk, gl, targets_dev, targets_np, full, prefix, hub_pre):
+    def _planner(self, blk, gl, targets_dev, targets_np, full, prefix, hub_pre, hub_host):
         import torch
 
         n_nodes = gl.num_nodes
@@ -450,13 +458,10 @@ class LayerwiseEngine:
                 n_i = n_t
             elif full and n_t == n_nodes:
                 n_i = n_t
-                key = ("hubtotal", kernels.HUB_MIN_DEGREE)
-                if key not in gl._cache:
-                    with torch.cuda.stream(self.plan_stream):
-                        gl._cache[key] = int(hub_pre[n_nodes].item())
-                n_h = gl._cache[key]
+                n_h = int(hub_host[n_nodes])
             else:
                 ids = gl._cache.get("plan_idset")      # reused across batches and runs
+                gl.wait_rows(end if full else None, stream=self.plan_stream)
                 with torch.cuda.stream(self.plan_stream):
                     if ids is None:
                         ids = gl._cache["plan_idset"] = kernels.IdSet(n_nodes, self.dev)
@@ -585,7 +590,8 @@ class LayerwiseEngine:
                       _prefix_host(gl.in_degrees, targets_np))
         else:
             prefix = np.zeros(len(targets_np) + 1, dtype=np.int64)
-        hub_pre = self._hub_counter(gl, targets_dev, full) if blk.has_conv else None
+        hub_pre, hub_host = (self._hub_counter(gl, targets_dev, full) if blk.has_conv
+                             else (None, None))
         layer_mats, layer_spaces = self._layer_inputs(blk, gl, targets_dev, full)
         fused = self._fusions(blk)
         gat_cache = {}
@@ -598,28 +604,44 @@ class LayerwiseEngine:
         def execute(plan: _Plan):
             if self.probe is not None:
                 self.probe.mark(f"L{layer} plan->exec [{plan.start},{plan.end})")
-            if sink_store is None or plan.end - plan.start < 2 * self.sink_chunks:
+            # A batch may run as row chunks -- the kernels are row-invariant, so
+            # the bytes are identical -- (a) in the final block, so each finished
+            # chunk's device->host copy overlaps the next chunk, and (b) while the
+            # graph is still uploading, so a chunk starts as soon as its CSR rows
+            # have arrived.
+            cuts = {plan.start, plan.end}
+            if sink_store is not None and plan.end - plan.start >= 2 * self.sink_chunks:
+                cuts.update(int(c) for c in np.linspace(plan.start, plan.end,
+                                                        self.sink_chunks + 1).astype(np.int64))
+            if full and gl._pending:
+                cuts.update(hi for hi, _ in gl._pending if plan.start < hi < plan.end)
+            cuts = sorted(cuts)
+            if len(cuts) == 2:
                 self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
-                                hub_pre, gat_cache)
+                                gat_cache)
                 if sink_store is not None:
                     self.sink(sink_store, plan.start, plan.end)
                 return
-            # Final block: run the batch as row chunks (row-invariant kernels, so
-            # identical bytes) and hand each finished chunk to the sink, which
-            # overlaps its device->host copy with the next chunk's kernels.
-            cuts = np.linspace(plan.start, plan.end, self.sink_chunks + 1).astype(np.int64)
-            hubs = (hub_pre[torch.from_numpy(cuts).to(self.dev)].cpu().numpy()
-                    if hub_pre is not None else np.zeros_like(cuts))
-            for k in range(self.sink_chunks):
-                lo, hi = int(cuts[k]), int(cuts[k + 1])
+            if hub_host is not None:
+                hubs = hub_host[np.asarray(cuts)]
+            elif hub_pre is not None:
+                hubs = hub_pre[torch.as_tensor(cuts, device=self.dev)].cpu().numpy()
+            else:
+                hubs = np.zeros(len(cuts), dtype=np.int64)
+            for k in range(len(cuts) - 1):
+                lo, hi = cuts[k], cuts[k + 1]
                 sub = _Plan(lo, hi, plan.num_inputs, int(prefix[hi] - prefix[lo]),
                             int(hubs[k + 1] - hubs[k]))
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
-                                hub_pre, gat_cache)
-                self.sink(sink_store, lo, hi)
+                                gat_cache)
+                if sink_store is not None:
+                    self.sink(sink_store, lo, hi)
 
-        self.plan_stream.wait_stream(torch.cuda.current_stream(self.dev))
-        plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix, hub_pre)
+        if full:
+            self.plan_stream.wait_event(gl.indptr_event)     # planning reads only the CSR
+        else:   # target lists / hub prefix were produced on the main stream
+            self.plan_stream.wait_stream(torch.cuda.current_stream(self.dev))
+        plan_fn = self._planner(blk, gl, targets_dev, targets_np, full, prefix, hub_pre, hub_host)
         sub_targets = targets_np[lo:hi] if (lo, hi) != (0, len(targets_np)) else targets_np
         sub_prefix = prefix[lo:hi + 1] - prefix[lo] if (lo, hi) != (0, len(targets_np)) else prefix
 
@@ -635,12 +657,14 @@ class LayerwiseEngine:
         return records
 
     def _run_batch(self, blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
-                   hub_pre, gat_cache):
+                   gat_cache):
         import torch
 
         m = self.m
         s, e = plan.start, plan.end
         B = e - s
+        if blk.has_conv:
+            gl.wait_rows(e if full else None)   # CSR rows of an in-flight upload
         if B == 0:
             return
         row_ids = None if full else targets_dev[s:e]
@@ -1035,13 +1059,39 @@ class InferenceResult:
     budget: object = None
 
 
-def _as_device_store(x, device) -> DeviceStore:
+def _host_tensor_ok(x) -> bool:
+    """Features that live on the host (numpy / EmbeddingStore / CPU tensor)."""
+    import torch
+
+    if isinstance(x, DeviceStore):
+        return False
+    if isinstance(x, torch.Tensor):
+        return not x.is_cuda
+    return True
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(device):
+    import torch
+
+    s = _COPY_STREAMS.get(device)
+    if s is None:
+        s = _COPY_STREAMS[device] = torch.cuda.Stream(device=device)
+    return s
+
+
+def _as_device_store(x, device, non_blocking=False) -> DeviceStore:
     import torch
 
     if isinstance(x, DeviceStore):
         return x
     arr = x.to_array() if isinstance(x, EmbeddingStore) else x
-    t = kernels.to_device(arr, torch.float32, device)
+    if non_blocking and isinstance(arr, torch.Tensor) and arr.dtype == torch.float32:
+        t = arr.to(kernels.cuda_device(device), non_blocking=True)
+    else:
+        t = kernels.to_device(arr, torch.float32, device)
     n, d = int(t.shape[0]), int(t.shape[1])
     if d % 4 == 0 and t.is_contiguous():
         return DeviceStore(n, d, t.device, data=t)
@@ -1150,8 +1200,23 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         x_store, (torch.Tensor, DeviceStore)))
 
     node_order = make_order(g, order, seed)
-    dg0 = kernels.device_graph(g)
-    x0 = _as_device_store(x_store, dg0.device)
+    if isinstance(g, CscGraph) and _host_tensor_ok(x_store):
+        # Host inputs: features first, then the CSR in row chunks on a copy
+        # stream; layer-1 batches start as soon as their rows have arrived.
+        dev = kernels.cuda_device()
+        copy = _copy_stream(dev)
+        copy.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(copy):
+            x0 = _as_device_store(x_store, dev, non_blocking=True)
+            x_ready = torch.cuda.Event()
+            x_ready.record(copy)
+        dg0 = DeviceGraph.upload_async(g, dev, copy)
+        torch.cuda.current_stream(dev).wait_event(x_ready)
+        if not node_order.is_identity():
+            dg0.wait_rows()
+    else:
+        dg0 = kernels.device_graph(g)
+        x0 = _as_device_store(x_store, dg0.device)
     g_i, x_i = apply_order_device(dg0, x0, node_order)
     if mode == "full" or targets is None:
         internal = user_targets                      # sorted(inv[arange(N)]) == arange(N)
