@@ -880,20 +880,28 @@ class KernelProbe:
         self.records.append((name, nbytes, start, ev))
         self._open = None
 
-    def mark(self, name):
-        """Timeline marker on the current stream (batch / layer boundaries)."""
+    def mark(self, name, stream=None):
+        """Timeline marker on `stream` (default current): device event + host time."""
         import torch
 
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
-        self.marks.append((name, ev))
+        ev.record(stream)
+        self.marks.append((name, ev, time.perf_counter()))
 
     def timeline(self):
-        """[(name, ms since previous marker)] (call after synchronize)."""
+        """[(name, device ms since previous marker)] (call after synchronize)."""
         out = []
-        for (_, e0), (name, e1) in zip(self.marks, self.marks[1:]):
+        for (_, e0, _), (name, e1, _) in zip(self.marks, self.marks[1:]):
             out.append((name, e0.elapsed_time(e1)))
         return out
+
+    def absolute(self):
+        """[(name, device ms since first marker, host ms since first marker)]."""
+        if not self.marks:
+            return []
+        e0, h0 = self.marks[0][1], self.marks[0][2]
+        return [(n, round(e0.elapsed_time(e), 3), round(1e3 * (h - h0), 3))
+                for n, e, h in self.marks]
 
     def summary(self):
         """{name: (launches, total bytes, total ms)} (call after synchronize)."""
@@ -1159,7 +1167,8 @@ def _exchange_for(distributed, mode, g):
 def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanout=None, seed=0,
                   executor="layerwise", order="none", budget=None, thresholds=None,
                   batch_size=1024, store_backing="memory", workdir=None, output="auto",
-                  precision=None, distributed="auto", reassociate=True) -> InferenceResult:
+                  precision=None, distributed="auto", reassociate=True,
+                  probe=None) -> InferenceResult:
     """End to end: reorder, annotate, execute, de-permute (glint/executor.py:481-543).
 
     ``budget`` may be a DeviceBudget (reference behaviour) or ``"device"``:
@@ -1199,6 +1208,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     host_out = (output == "numpy") or (output == "auto" and not isinstance(
         x_store, (torch.Tensor, DeviceStore)))
 
+    if probe is not None:
+        probe.mark("run_inference entry")
     node_order = make_order(g, order, seed)
     if isinstance(g, CscGraph) and _host_tensor_ok(x_store):
         # Host inputs: features first, then the CSR in row chunks on a copy
@@ -1210,7 +1221,12 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             x0 = _as_device_store(x_store, dev, non_blocking=True)
             x_ready = torch.cuda.Event()
             x_ready.record(copy)
+            if probe is not None:
+                probe.mark("features uploaded (copy stream)", copy)
         dg0 = DeviceGraph.upload_async(g, dev, copy)
+        if probe is not None:
+            probe.mark("csr uploaded (copy stream)", copy)
+            probe.mark("uploads issued (main stream)")
         torch.cuda.current_stream(dev).wait_event(x_ready)
         if not node_order.is_identity():
             dg0.wait_rows()
@@ -1242,6 +1258,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
                 and len(row_ids) == g.num_nodes and user_targets is arange_ids(g.num_nodes)):
             streamed = _HostSink(g.num_nodes, m.output_dim, dg0.device)
             eng.sink = streamed
+        eng.probe = probe
         store = eng.run(exchange=ex)
         if ex is not None:
             ex.exchange_tensor(store.data)      # every rank returns the full output
@@ -1255,6 +1272,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         row_ids = internal
         out_dev = _gather_dense(out_sorted, row_ids, node_order.inv[user_targets])
     if executor == "layerwise" and streamed is not None:
+        if probe is not None:
+            probe.mark("output streamed (copy stream)", streamed.stream)
         output_val = streamed.finish()
     elif host_out:
         staging = torch.empty(tuple(out_dev.shape), dtype=torch.float32, pin_memory=True)
