@@ -601,41 +601,51 @@ class LayerwiseEngine:
         sink_store = (self.stores.get(out_key) if self.sink is not None
                       and blk.block_id == self.schedule.model_output.block else None)
 
-        def execute(plan: _Plan):
-            if self.probe is not None:
-                self.probe.mark(f"L{layer} plan->exec [{plan.start},{plan.end})")
-            # A batch may run as row chunks -- the kernels are row-invariant, so
-            # the bytes are identical -- (a) in the final block, so each finished
-            # chunk's device->host copy overlaps the next chunk, and (b) while the
-            # graph is still uploading, so a chunk starts as soon as its CSR rows
-            # have arrived.
-            cuts = {plan.start, plan.end}
-            if sink_store is not None and plan.end - plan.start >= 2 * self.sink_chunks:
-                cuts.update(int(c) for c in np.linspace(plan.start, plan.end,
-                                                        self.sink_chunks + 1).astype(np.int64))
+        def run_rows(r0, r1, n_inputs):
+            # Rows [r0, r1) may run as row chunks -- the kernels are row-invariant,
+            # so the bytes are identical -- (a) in the final block, so each
+            # finished chunk's device->host copy overlaps the next chunk, and (b)
+            # while the graph is still uploading, so a chunk starts as soon as its
+            # CSR rows have arrived.
+            cuts = {r0, r1}
+            if sink_store is not None and r1 - r0 >= 2 * self.sink_chunks:
+                cuts.update(int(c) for c in np.linspace(r0, r1, self.sink_chunks + 1)
+                            .astype(np.int64))
             if full and gl._pending:
-                cuts.update(hi for hi, _ in gl._pending if plan.start < hi < plan.end)
+                cuts.update(h for h, _ in gl._pending if r0 < h < r1)
             cuts = sorted(cuts)
-            if len(cuts) == 2:
-                self._run_batch(blk, gl, plan, full, targets_dev, layer_mats, layer_spaces, fused,
-                                gat_cache)
-                if sink_store is not None:
-                    self.sink(sink_store, plan.start, plan.end)
-                return
             if hub_host is not None:
                 hubs = hub_host[np.asarray(cuts)]
-            elif hub_pre is not None:
+            elif hub_pre is not None and len(cuts) > 2:
                 hubs = hub_pre[torch.as_tensor(cuts, device=self.dev)].cpu().numpy()
             else:
-                hubs = np.zeros(len(cuts), dtype=np.int64)
+                hubs = None
             for k in range(len(cuts) - 1):
-                lo, hi = cuts[k], cuts[k + 1]
-                sub = _Plan(lo, hi, plan.num_inputs, int(prefix[hi] - prefix[lo]),
-                            int(hubs[k + 1] - hubs[k]))
+                c0, c1 = cuts[k], cuts[k + 1]
+                n_hub = int(hubs[k + 1] - hubs[k]) if hubs is not None else self._batch_hubs
+                sub = _Plan(c0, c1, n_inputs, int(prefix[c1] - prefix[c0]), n_hub)
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
                                 gat_cache)
                 if sink_store is not None:
-                    self.sink(sink_store, lo, hi)
+                    self.sink(sink_store, c0, c1)
+
+        # Speculation while the CSR is still uploading (full mode): a batch's rows
+        # are launched before its planning count blocks the host (the count needs
+        # the batch's edge ids, i.e. the whole upload for the last layer-1
+        # batch).  Batch invariance makes early (or repeated, after an OOM
+        # retry shrinks a batch) computation of a row harmless; planning and the
+        # batch records are untouched.
+        spec = {"hi": lo}
+        speculate = (full and blk.has_conv and bool(gl._pending)
+                     and not gl._pending[-1][1].query())
+
+        def execute(plan: _Plan):
+            if self.probe is not None:
+                self.probe.mark(f"L{layer} plan->exec [{plan.start},{plan.end})")
+            self._batch_hubs = plan.num_hubs
+            r0 = max(plan.start, spec["hi"]) if speculate else plan.start
+            if r0 < plan.end:
+                run_rows(r0, plan.end, plan.num_inputs)
 
         if full:
             self.plan_stream.wait_event(gl.indptr_event)     # planning reads only the CSR
@@ -646,7 +656,11 @@ class LayerwiseEngine:
         sub_prefix = prefix[lo:hi + 1] - prefix[lo] if (lo, hi) != (0, len(targets_np)) else prefix
 
         def plan_off(start, end):
-            plan, fp = plan_fn(start + lo, end + lo)
+            a, b = start + lo, end + lo
+            if speculate and b > spec["hi"]:
+                run_rows(max(a, spec["hi"]), b, b - a)
+                spec["hi"] = b
+            plan, fp = plan_fn(a, b)
             return plan, fp
 
         records = self.controller.run_layer(layer, sub_targets, sub_prefix, plan_off, execute)
@@ -1216,14 +1230,17 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         # stream; layer-1 batches start as soon as their rows have arrived.
         dev = kernels.cuda_device()
         copy = _copy_stream(dev)
-        copy.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(copy):
-            x0 = _as_device_store(x_store, dev, non_blocking=True)
-            x_ready = torch.cuda.Event()
-            x_ready.record(copy)
+        box = {}
+
+        def upload_features():          # queued right after indptr, before the CSR
+            box["x"] = _as_device_store(x_store, dev, non_blocking=True)
+            box["ev"] = torch.cuda.Event()
+            box["ev"].record(copy)
             if probe is not None:
                 probe.mark("features uploaded (copy stream)", copy)
-        dg0 = DeviceGraph.upload_async(g, dev, copy)
+
+        dg0 = DeviceGraph.upload_async(g, dev, copy, after_indptr=upload_features)
+        x0, x_ready = box["x"], box["ev"]
         if probe is not None:
             probe.mark("csr uploaded (copy stream)", copy)
             probe.mark("uploads issued (main stream)")
