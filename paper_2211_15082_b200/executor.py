@@ -611,7 +611,7 @@ class LayerwiseEngine:
             if sink_store is not None and r1 - r0 >= 2 * self.sink_chunks:
                 cuts.update(int(c) for c in np.linspace(r0, r1, self.sink_chunks + 1)
                             .astype(np.int64))
-            if full and gl._pending:
+            if full and gl.upload_in_flight():
                 cuts.update(h for h, _ in gl._pending if r0 < h < r1)
             cuts = sorted(cuts)
             if hub_host is not None:
@@ -636,8 +636,7 @@ class LayerwiseEngine:
         # retry shrinks a batch) computation of a row harmless; planning and the
         # batch records are untouched.
         spec = {"hi": lo}
-        speculate = (full and blk.has_conv and bool(gl._pending)
-                     and not gl._pending[-1][1].query())
+        speculate = full and blk.has_conv and gl.upload_in_flight()
 
         def execute(plan: _Plan):
             if self.probe is not None:
