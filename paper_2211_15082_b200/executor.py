@@ -385,7 +385,7 @@ class LayerwiseEngine:
         self.kernel_launches = 0
         self.probe = None               # optional KernelProbe (bench roofline timing)
         self.sink = None                # optional sink(store, row_lo, row_hi) for final rows
-        self.sink_chunks = 4
+        self.sink_chunks = 2            # each chunk is bounded by its slowest hub row
 
     # -- helpers ------------------------------------------------------------
 
