@@ -71,6 +71,7 @@ int glint_abi_version(void);
 #define GLINT_TUNE_GEMM_PROF 1    /* 1: K2 tcgen05 kernel accumulates phase cycles */
 #define GLINT_TUNE_HUB_INLINE 2   /* K1 hub rows: 0 auto, 1 register path in the main
                                      kernel, 2 bulk-copy kernel on a side stream */
+#define GLINT_TUNE_GAT_VARIANT 3  /* K4 launch variant (occupancy / unroll) */
 #define GLINT_TUNE_COUNT 8
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);

@@ -35,6 +35,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kHubChunk = 1024;  // staged source offsets per hub iteration
 constexpr int kHubUnroll = 32;   // loads in flight per thread on the hub path
 constexpr int kMaxHeads = 8;
+constexpr int LPR_MIN = 8;  // narrowest lane group of the GAT kernel
 
 struct RowAddr {
   const int64_t* __restrict__ indptr;
@@ -573,52 +574,51 @@ __device__ __forceinline__ float leaky(float x, float slope) {
   return x >= 0.0f ? x : __fmul_rn(slope, x);
 }
 
-// Regular GAT row: one warp, lanes over 128-bit chunks of the head-padded Z row.
-template <int VPL, int U>
-__device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int lane,
-                                                float (*w_s)[kMaxHeads]) {
+// Regular GAT row: a group of LPR lanes owns one row; lane g covers the
+// 128-bit chunks g, g+LPR, ... of the head-padded Z row.  H (heads) is a
+// compile-time constant so per-head state stays in registers.
+//   pass 1: per-head peak over self + edges (lanes over edges, order-free max);
+//   pass 2: per chunk of LPR edges, lane i computes the H softmax weights of
+//           edge i once into shared memory (w_s[i][h]), then every lane walks
+//           the chunk in stored edge order with U neighbour-row loads in
+//           flight: den += w; num += w*z (mul then add, as numpy), self last.
+template <int H, int LPR, int VPL, int U>
+__device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int lane_g,
+                                                unsigned gmask, float* w_s, float* st) {
+  // st: per-group scratch, st[h] = s_dst[self][h], st[H + h] = peak[h]
   const int64_t rid = a.ra.csr_row(r);
   const int64_t beg = a.ra.indptr[rid];
   const int64_t end = a.ra.indptr[rid + 1];
   const int64_t self = a.ra.self_row(r, rid);
-  const int H = a.heads;
-
-  float sdst[kMaxHeads], peak[kMaxHeads], wself[kMaxHeads];
+  {
+    float sdst[H], peak[H];
 #pragma unroll
-  for (int h = 0; h < kMaxHeads; ++h) {
-    if (h < H) {
-      sdst[h] = a.s_dst[self * H + h];
-      peak[h] = leaky(__fadd_rn(a.s_src[self * H + h], sdst[h]), a.slope);
-      wself[h] = peak[h];  // self logit, fixed up below
+    for (int h = 0; h < H; ++h) {
+      sdst[h] = __ldg(a.s_dst + self * H + h);
+      peak[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope);
     }
-  }
-  // pass 1: per-head max over edges (lanes over edges, order-free)
-  for (int64_t e = beg + lane; e < end; e += 32) {
-    const int64_t u = a.ra.map(a.ra.indices[e]);
+    for (int64_t e = beg + lane_g; e < end; e += LPR) {
+      const int64_t u = a.ra.map(a.ra.indices[e]);
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h)
-      if (h < H) peak[h] = fmaxf(peak[h], leaky(__fadd_rn(a.s_src[u * H + h], sdst[h]), a.slope));
-  }
-#pragma unroll
-  for (int h = 0; h < kMaxHeads; ++h) {
-    if (h < H) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) peak[h] = fmaxf(peak[h], __shfl_xor_sync(0xffffffffu, peak[h], o));
-      wself[h] = expf(__fsub_rn(wself[h], peak[h]));
+      for (int h = 0; h < H; ++h)
+        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(__ldg(a.s_src + u * H + h), sdst[h]), a.slope));
     }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1)
+        peak[h] = fmaxf(peak[h], __shfl_xor_sync(gmask, peak[h], o, LPR));
+    }
+    if (lane_g == 0) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        st[h] = sdst[h];
+        st[H + h] = peak[h];
+      }
+    }
+    __syncwarp(gmask);
   }
 
-  // lane's chunk -> head mapping
-  int head_of[VPL], j_of[VPL];
-  bool valid_chunk[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int zc = (lane + 32 * k) * 4;
-    head_of[k] = zc / a.head_pitch;
-    j_of[k] = zc - head_of[k] * a.head_pitch;
-    valid_chunk[k] = head_of[k] < H;
-    if (!valid_chunk[k]) head_of[k] = 0;
-  }
   float num[VPL][4], den[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -626,35 +626,39 @@ __device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int
 #pragma unroll
     for (int c = 0; c < 4; ++c) num[k][c] = 0.0f;
   }
+  const int head0 = (lane_g * 4) / a.head_pitch;  // head of chunk k is (zc_k / head_pitch)
 
-  for (int64_t e0 = beg; e0 < end; e0 += 32) {
-    const int cnt = static_cast<int>(min(static_cast<int64_t>(32), end - e0));
+  for (int64_t e0 = beg; e0 < end; e0 += LPR) {
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(LPR), end - e0));
     int64_t my = 0;
-    if (lane < cnt) {
-      const int64_t u = a.ra.map(a.ra.indices[e0 + lane]);
+    if (lane_g < cnt) {
+      const int64_t u = a.ra.map(a.ra.indices[e0 + lane_g]);
       my = u * a.ldz;
 #pragma unroll
-      for (int h = 0; h < kMaxHeads; ++h)
-        if (h < H)
-          w_s[lane][h] = expf(__fsub_rn(leaky(__fadd_rn(a.s_src[u * H + h], sdst[h]), a.slope), peak[h]));
+      for (int h = 0; h < H; ++h)
+        w_s[lane_g * H + h] = expf(
+            __fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + u * H + h), st[h]), a.slope), st[H + h]));
     }
-    __syncwarp();
+    __syncwarp(gmask);
     for (int j = 0; j < cnt; j += U) {
       float4 v[U][VPL];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t off = shfl64(0xffffffffu, my, (j + u) & 31, 32);
+        const int64_t off = shfl64(gmask, my, (j + u) & (LPR - 1), LPR);
 #pragma unroll
-        for (int k = 0; k < VPL; ++k)
-          v[u][k] = (j + u < cnt && valid_chunk[k]) ? ldg_f4(a.Z + off + (lane + 32 * k) * 4)
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < VPL; ++k) {
+          const int zc = (lane_g + LPR * k) * 4;
+          v[u][k] = (j + u < cnt && zc < H * a.head_pitch) ? ldg_f4(a.Z + off + zc)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (j + u < cnt) {
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
-            const float w = w_s[j + u][head_of[k]];
+            const int hk = ((lane_g + LPR * k) * 4) / a.head_pitch;
+            const float w = w_s[(j + u) * H + (hk < H ? hk : 0)];
             den[k] = __fadd_rn(den[k], w);
             num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v[u][k].x));
             num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v[u][k].y));
@@ -664,25 +668,25 @@ __device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int
         }
       }
     }
-    __syncwarp();
+    __syncwarp(gmask);
   }
+  (void)head0;
   // self term last, then normalise and write the unpadded head columns
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
-    if (!valid_chunk[k]) continue;
-    const int hh = head_of[k];
-    const float4 zs = ldg_f4(a.Z + self * a.ldz + (lane + 32 * k) * 4);
-    const float ws = wself[hh];
+    const int zc = (lane_g + LPR * k) * 4;
+    const int hh = zc / a.head_pitch;
+    if (hh >= H) continue;
+    const int jc = zc - hh * a.head_pitch;
+    const float4 zs = ldg_f4(a.Z + self * a.ldz + zc);
+    const float ws = expf(__fsub_rn(
+        leaky(__fadd_rn(__ldg(a.s_src + self * H + hh), st[hh]), a.slope), st[H + hh]));
     const float d = __fadd_rn(den[k], ws);
     const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
+    float* dst = a.out + r * a.ld_out + hh * a.head_dim + jc;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j_of[k] + c;
-      if (j < a.head_dim) {
-        const float n = __fadd_rn(num[k][c], __fmul_rn(ws, zv[c]));
-        a.out[r * a.ld_out + hh * a.head_dim + j] = __fdiv_rn(n, d);
-      }
-    }
+    for (int c = 0; c < 4; ++c)
+      if (jc + c < a.head_dim) dst[c] = __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d);
   }
 }
 
@@ -759,33 +763,97 @@ __device__ __forceinline__ void gat_row_hub(const GatArgs& a, int64_t r, int col
   }
 }
 
-template <int VPL, int U>
-__global__ void __launch_bounds__(kThreads) gat_kernel(GatArgs a) {
+// Hub rows (first n_hub schedule entries): one CTA per (row, 256-column block).
+__global__ void __launch_bounds__(kThreads) gat_hub_kernel(GatArgs a) {
   __shared__ int64_t s_off[kGatHubChunk];
   __shared__ float s_w[kGatHubChunk][kMaxHeads];
   __shared__ float s_peak[kMaxHeads];
-  if (static_cast<int64_t>(blockIdx.x) < a.sc.hub_ctas) {
-    const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
-    const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
-    gat_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off, s_w, s_peak);
-    return;
-  }
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t idx = a.sc.n_hub + (static_cast<int64_t>(blockIdx.x) - a.sc.hub_ctas) * kWarps + warp;
-  if (idx >= a.sc.n_rows) return;
-  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
-  // regular rows reuse the hub staging buffer as per-warp weight tiles
-  float(*w_s)[kMaxHeads] = s_w + warp * 32;
-  gat_row_regular<VPL, U>(a, r, lane, w_s);
+  const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
+  const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
+  gat_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off, s_w, s_peak);
 }
 
-template <int VPL, int U>
+// Regular rows (schedule entries n_hub..n_rows), LPR lanes per row.
+template <int H, int LPR, int VPL, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) gat_kernel(GatArgs a) {
+  __shared__ float s_w[kThreads * H];
+  __shared__ float s_st[kThreads / LPR_MIN][2 * H];
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
+  const int64_t idx = a.sc.n_hub + slot;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  float* w_s = s_w + (warp * 32 + group * LPR) * H;  // LPR x H weights per lane group
+  gat_row_regular<H, LPR, VPL, U>(a, r, lane_g, gmask, w_s, s_st[warp * G + group]);
+}
+
+template <int H, int LPR, int VPL, int U, int MINB>
 int launch_gat(const GatArgs& a, cudaStream_t s) {
-  const int64_t grid = a.sc.hub_ctas + ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps);
-  if (grid <= 0) return GLINT_OK;
-  gat_kernel<VPL, U><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
-  return launch_status("gat_aggregate");
+  constexpr int G = 32 / LPR;
+  const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
+  SideStream* ss = nullptr;
+  if (a.sc.hub_ctas > 0) {
+    // hub CTAs on the library side stream, concurrent with the regular rows
+    int rc = side_stream(&ss);
+    if (rc) return rc;
+    GLINT_CUDA(cudaEventRecord(ss->fork, s));
+    GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
+    gat_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
+    rc = launch_status("gat_aggregate_hub");
+    if (rc) return rc;
+    GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
+  }
+  if (grid > 0) gat_kernel<H, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  const int rc = launch_status("gat_aggregate");
+  if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+  return rc;
+}
+
+// chunks = 128-bit chunks per padded Z row.  Variants (GLINT_TUNE_GAT_VARIANT)
+// trade unroll depth against occupancy; 0 = default (best measured).
+template <int H>
+int dispatch_gat_h(const GatArgs& a, int chunks, cudaStream_t s) {
+  const int v = tuning(GLINT_TUNE_GAT_VARIANT);
+  if (chunks <= 8) return launch_gat<H, 8, 1, 4, 6>(a, s);
+  if (chunks <= 16) return launch_gat<H, 16, 1, 4, 6>(a, s);
+  if (chunks <= 32) {
+    if (v == 1) return launch_gat<H, 32, 1, 8, 4>(a, s);
+    if (v == 2) return launch_gat<H, 16, 2, 4, 5>(a, s);
+    return launch_gat<H, 32, 1, 4, 6>(a, s);
+  }
+  if (chunks <= 48) {
+    if (v == 1) return launch_gat<H, 16, 3, 3, 3>(a, s);
+    if (v == 2) return launch_gat<H, 32, 2, 3, 4>(a, s);
+    if (v == 3) return launch_gat<H, 16, 3, 2, 5>(a, s);
+    return launch_gat<H, 16, 3, 2, 4>(a, s);
+  }
+  if (chunks <= 64) {
+    if (v == 1) return launch_gat<H, 32, 2, 4, 3>(a, s);
+    if (v == 2) return launch_gat<H, 32, 2, 2, 5>(a, s);
+    if (v == 3) return launch_gat<H, 32, 2, 4, 4>(a, s);
+    if (v == 4) return launch_gat<H, 32, 2, 3, 5>(a, s);
+    return launch_gat<H, 32, 2, 3, 4>(a, s);
+  }
+  if (chunks <= 128) return launch_gat<H, 32, 4, 2, 3>(a, s);
+  return launch_gat<H, 32, 8, 1, 2>(a, s);
+}
+
+int dispatch_gat(const GatArgs& a, int chunks, cudaStream_t s) {
+  switch (a.heads) {
+    case 1: return dispatch_gat_h<1>(a, chunks, s);
+    case 2: return dispatch_gat_h<2>(a, chunks, s);
+    case 3: return dispatch_gat_h<3>(a, chunks, s);
+    case 4: return dispatch_gat_h<4>(a, chunks, s);
+    case 5: return dispatch_gat_h<5>(a, chunks, s);
+    case 6: return dispatch_gat_h<6>(a, chunks, s);
+    case 7: return dispatch_gat_h<7>(a, chunks, s);
+    default: return dispatch_gat_h<8>(a, chunks, s);
+  }
 }
 
 }  // namespace
@@ -891,11 +959,8 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
   a.sc.hub_ctas = n_hub * a.sc.hub_col_blocks;
   const int chunks = zw / 4;
   cudaStream_t s = as_stream(stream);
-  if (chunks <= 32) return launch_gat<1, 8>(a, s);
-  if (chunks <= 64) return launch_gat<2, 4>(a, s);
-  if (chunks <= 128) return launch_gat<4, 2>(a, s);
   GLINT_REQUIRE(chunks <= 256, "gat_aggregate: heads*head_pitch must be <= 1024");
-  return launch_gat<8, 2>(a, s);
+  return dispatch_gat(a, chunks, s);
 }
 
 }  // extern "C"

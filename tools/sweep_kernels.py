@@ -49,7 +49,8 @@ def main():
     args = ap.parse_args()
     n = args.nodes
     und = int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES))
-    g = synth.gen_products_like(n, und, seed=0, device="cuda") if "spmm" in args.what else None
+    g = synth.gen_products_like(n, und, seed=0, device="cuda") \
+        if ("spmm" in args.what or "gat" in args.what) else None
     if g is None:
         gemm_only(args, n)
         return
@@ -59,6 +60,8 @@ def main():
     assert int(nh.item()) == hub_pre
     print(json.dumps({"graph": {"nodes": n, "edges": g.num_edges, "max_deg": int(deg.max()),
                                 "hubs": hub_pre}}), flush=True)
+    if "gat" in args.what:
+        sweep_gat(args, g, n)
     dims = [int(x) for x in args.dims.split(",")] if "spmm" in args.what else []
     for d in dims:
         h = torch.randn((n, d), device="cuda")
@@ -132,6 +135,44 @@ def main():
         err = float((res[0] - res[1]).norm() / res[0].norm())
         print(json.dumps({"kernel": "linear_agree", "K": K, "N": N, "rel_l2_fp32_vs_3xtf32": err}))
         del a, c
+
+
+def sweep_gat(args, g, n):
+    """K4 (GAT edge-softmax aggregation) variants at the cfg3 widths (4 heads x 64 / 47)."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+    from paper_2211_15082_b200.executor import agg_bytes
+
+    heads = 4
+    sched, nh = kernels.degree_schedule(g.indptr, None, 0, n)
+    n_hub = int(nh.item())
+    for dh in (64, 47):
+        hp = kernels.head_pitch(dh)
+        Z = torch.randn((n, heads * hp), device="cuda")
+        s_src = torch.randn((n, heads), device="cuda")
+        s_dst = torch.randn((n, heads), device="cuda")
+        out = torch.empty((n, heads * dh), device="cuda")
+        ref = None
+        for variant in range(args.variants):
+            _lib.call("glint_set_tuning", 3, variant)
+
+            def run():
+                kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, g.indptr, g.indices, n,
+                                      schedule=sched, n_hub=n_hub)
+
+            ms = timed(run, args.reps)
+            nb = agg_bytes(heads * hp, g.num_edges, n, heads=heads)
+            same = None
+            if ref is None:
+                ref = out.clone()
+            else:
+                same = bool(torch.equal(ref, out))
+            print(json.dumps({"kernel": "gat_aggregate", "heads": heads, "head_dim": dh,
+                              "variant": variant, "ms": ms, "GBps": nb / ms / 1e6,
+                              "identical_to_v0": same}), flush=True)
+        _lib.call("glint_set_tuning", 3, 0)
+        del Z, out, ref
 
 
 def gemm_only(args, n):
