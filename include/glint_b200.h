@@ -149,7 +149,9 @@ int glint_gat_scores_f32(int64_t M, int32_t heads, int32_t head_dim,
  * w = exp(logit - peak); out[r, h*head_dim + j] =
  *   (sum_e w_e * z_h[u_e, j] (stored order) + w_self * z_h[v, j]) /
  *   (sum_e w_e + w_self).  Row addressing as glint_spmm_mean_f32; the
- * self row of Z / s_* is `self`, the source rows map(u). */
+ * self row of Z / s_* is `self`, the source rows map(u).  act (GLINT_ACT_*)
+ * is applied to each output element (the model's following ReLU fused into
+ * the epilogue; GLINT_ACT_NONE = the reference op alone). */
 int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim,
                             int32_t head_pitch, const int64_t* indptr,
                             const int32_t* indices, const int64_t* row_ids,
@@ -157,7 +159,7 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim,
                             const int32_t* col_map, const float* Z, int64_t ldz,
                             const float* s_src, const float* s_dst, float slope,
                             float* out, int64_t ld_out, const int32_t* schedule,
-                            int64_t n_hub, glint_stream_t stream);
+                            int64_t n_hub, int32_t act, glint_stream_t stream);
 
 /* --------------------------------------------------- K5 per-row operators
  * Replaces kernels.py:206-231 elementwise.  inputs / ld_inputs / input_rows

@@ -50,7 +50,7 @@ SIGNATURES = {
     "glint_gat_scores_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P]),
     "glint_gat_aggregate_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _P, _P, _I64, _P,
                                                _P, _P, _I64, _P, _P, _F32, _P, _I64, _P, _I64,
-                                               _P]),
+                                               _I32, _P]),
     "glint_elementwise_f32": (ctypes.c_int, [_I32, _I64, _I32, _I32, _P, _P, _P, _P, _I64, _P]),
     "glint_copy_rows_f32": (ctypes.c_int, [_I64, _I32, _P, _I64, _P, _P, _I64, _P, _P]),
     "glint_idset_workspace_bytes": (_SZ, [_I64]),

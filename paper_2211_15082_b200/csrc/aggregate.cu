@@ -568,7 +568,14 @@ struct GatArgs {
   float slope;
   float* __restrict__ out;
   int64_t ld_out;
+  int act;
 };
+
+__device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
+  if (a.act == GLINT_ACT_RELU) v = (v > 0.0f || v != v) ? v : 0.0f;
+  if (a.act == GLINT_ACT_LEAKY_RELU) v = v >= 0.0f ? v : __fmul_rn(0.2f, v);
+  return v;
+}
 
 __device__ __forceinline__ float leaky(float x, float slope) {
   return x >= 0.0f ? x : __fmul_rn(slope, x);
@@ -686,7 +693,8 @@ __device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int
     float* dst = a.out + r * a.ld_out + hh * a.head_dim + jc;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (jc + c < a.head_dim) dst[c] = __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d);
+      if (jc + c < a.head_dim)
+        dst[c] = gat_epilogue(a, __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d));
   }
 }
 
@@ -759,7 +767,7 @@ __device__ __forceinline__ void gat_row_hub(const GatArgs& a, int64_t r, int col
                                     s_peak[hs]));
     const float d = __fadd_rn(den, ws);
     const float n = __fadd_rn(num, __fmul_rn(ws, __ldg(a.Z + self * a.ldz + zc)));
-    a.out[r * a.ld_out + hh * a.head_dim + j] = __fdiv_rn(n, d);
+    a.out[r * a.ld_out + hh * a.head_dim + j] = gat_epilogue(a, __fdiv_rn(n, d));
   }
 }
 
@@ -771,6 +779,201 @@ __global__ void __launch_bounds__(kThreads) gat_hub_kernel(GatArgs a) {
   const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
   const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
   gat_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off, s_w, s_peak);
+}
+
+// Hub rows, bulk-copy ring (as mean_hub_kernel): one CTA per (hub row,
+// 64-column slice of the padded Z row).  Warp 2 streams the slice of every
+// source row into a 64 KB shared ring with cp.async.bulk; warps 0-1 (one
+// column per thread) first reduce the per-head peak over self + all edges,
+// then, per chunk of kGatWChunk edges, compute the chunk's softmax weights
+// into shared memory (consumer-only named barrier) and walk the ring in
+// stored edge order: den += w, num += w*z, self last -- the same arithmetic
+// and order as gat_row_regular.
+constexpr int kGatWChunk = 2048;
+constexpr int kConsumers = kHubConsumerWarps * 32;
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
+}
+
+__global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, int slots_per_group,
+                                                                   int slice_floats,
+                                                                   int col_blocks) {
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full_bar[kHubGroups];
+  __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
+  __shared__ float s_sd[kMaxHeads], s_pk[kMaxHeads];
+  __shared__ float s_red[kHubConsumerWarps][kMaxHeads];
+  const int H = a.heads;
+  float* w_sm = ring + kHubGroups * slots_per_group * slice_floats;  // [kGatWChunk][H]
+  const int cb = static_cast<int>(blockIdx.x % col_blocks);
+  const int64_t r = a.sc.schedule[blockIdx.x / col_blocks];
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  const int zw = H * a.head_pitch;
+  const int c0 = cb * slice_floats;
+  const int width = min(slice_floats, zw - c0);
+  const uint32_t slice_bytes = static_cast<uint32_t>(((width + 3) / 4) * 16);
+  const int64_t deg = end - beg;
+  const int64_t ngroups = (deg + slots_per_group - 1) / slots_per_group;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < kHubGroups; ++g) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[g])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                   ::"r"(smem_u32(&empty_bar[g])), "r"(kHubConsumerWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kHubConsumerWarps) {
+    // producer: identical to mean_hub_kernel's
+    const int64_t ncycles = (ngroups + kHubGroups - 1) / kHubGroups;
+    auto load_cycle = [&](int64_t c, int64_t (&ids)[kHubGroups]) {
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) {
+        const int64_t e = beg + (c * kHubGroups + t) * slots_per_group + lane;
+        ids[t] = (lane < slots_per_group && e < end) ? a.ra.map(a.ra.indices[e]) : 0;
+      }
+    };
+    int64_t cur[kHubGroups], nxt[kHubGroups];
+    if (ncycles > 0) load_cycle(0, cur);
+    for (int64_t c = 0; c < ncycles; ++c) {
+      if (c + 1 < ncycles) load_cycle(c + 1, nxt);
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) {
+        const int64_t gi = c * kHubGroups + t;
+        if (gi < ngroups) {
+          if (c > 0) hub_mbar_wait(&empty_bar[t], static_cast<uint32_t>(c - 1) & 1u);
+          const int64_t e0 = beg + gi * slots_per_group;
+          const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
+          if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(smem_u32(&full_bar[t])), "r"(slice_bytes * cnt) : "memory");
+          }
+          __syncwarp();
+          if (lane < cnt) {
+            float* dst = ring + (static_cast<int64_t>(t) * slots_per_group + lane) * slice_floats;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                ::"r"(smem_u32(dst)), "l"(a.Z + cur[t] * a.ldz + c0), "r"(slice_bytes),
+                "r"(smem_u32(&full_bar[t]))
+                : "memory");
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kHubGroups; ++t) cur[t] = nxt[t];
+    }
+    return;
+  }
+
+  // consumers: per-head peak over self + edges (order-free max)
+  const int tid = threadIdx.x;
+  {
+    float sd[kMaxHeads], pk[kMaxHeads];
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+      if (h < H) {
+        sd[h] = __ldg(a.s_dst + self * H + h);
+        pk[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sd[h]), a.slope);
+      }
+    }
+    for (int64_t e = beg + tid; e < end; e += kConsumers) {
+      const int64_t u = a.ra.map(a.ra.indices[e]);
+#pragma unroll
+      for (int h = 0; h < kMaxHeads; ++h)
+        if (h < H) pk[h] = fmaxf(pk[h], leaky(__fadd_rn(__ldg(a.s_src + u * H + h), sd[h]), a.slope));
+    }
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+      if (h < H) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pk[h] = fmaxf(pk[h], __shfl_xor_sync(0xffffffffu, pk[h], o));
+        if (lane == 0) s_red[warp][h] = pk[h];
+        if (tid == 0) s_sd[h] = sd[h];
+      }
+    }
+    consumer_sync();
+    if (tid < H) {
+      float m = s_red[0][tid];
+      for (int w = 1; w < kHubConsumerWarps; ++w) m = fmaxf(m, s_red[w][tid]);
+      s_pk[tid] = m;
+    }
+    consumer_sync();
+  }
+  const int col = c0 + tid;
+  const int hh = min(col / a.head_pitch, H - 1);
+  const int jc = col - hh * a.head_pitch;
+  const bool active = tid < width && col < zw && jc < a.head_dim;
+  float num = 0.0f, den = 0.0f;
+  const int groups_per_chunk = kGatWChunk / slots_per_group;
+  for (int64_t gi = 0; gi < ngroups; ++gi) {
+    const int64_t wbase = (gi / groups_per_chunk) * kGatWChunk;
+    if (gi % groups_per_chunk == 0) {
+      // softmax weights of edges [beg + wbase, +kGatWChunk) for all heads
+      consumer_sync();
+      const int64_t e0 = beg + wbase;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(kGatWChunk), end - e0));
+      for (int t = tid; t < cnt; t += kConsumers) {
+        const int64_t u = a.ra.map(a.ra.indices[e0 + t]);
+        for (int h = 0; h < H; ++h)
+          w_sm[t * H + h] = expf(
+              __fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + u * H + h), s_sd[h]), a.slope), s_pk[h]));
+      }
+      consumer_sync();
+    }
+    const int g = static_cast<int>(gi % kHubGroups);
+    const uint32_t round = static_cast<uint32_t>(gi / kHubGroups);
+    hub_mbar_wait(&full_bar[g], round & 1u);
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group),
+                                         end - (beg + gi * slots_per_group)));
+    const float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
+    const float* wrow = w_sm + (gi * slots_per_group - wbase) * H + hh;
+    if (active) {
+      for (int j = 0; j < cnt; ++j) {
+        const float w = wrow[j * H];
+        den = __fadd_rn(den, w);
+        num = __fadd_rn(num, __fmul_rn(w, slot0[j * slice_floats + tid]));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
+                                ::"r"(smem_u32(&empty_bar[g])) : "memory");
+  }
+  if (active) {
+    const float ws = expf(__fsub_rn(
+        leaky(__fadd_rn(__ldg(a.s_src + self * H + hh), s_sd[hh]), a.slope), s_pk[hh]));
+    const float d = __fadd_rn(den, ws);
+    const float n = __fadd_rn(num, __fmul_rn(ws, __ldg(a.Z + self * a.ldz + col)));
+    a.out[r * a.ld_out + hh * a.head_dim + jc] = gat_epilogue(a, __fdiv_rn(n, d));
+  }
+}
+
+int launch_gat_hub_ring(const GatArgs& a, cudaStream_t s) {
+  const int zw = a.heads * a.head_pitch;
+  const int width = std::min(kHubSlice, zw);
+  const int slice_floats = ((width + 3) / 4) * 4;
+  const int col_blocks = static_cast<int>(ceil_div(zw, kHubSlice));
+  int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
+  per_group = std::max(1, std::min(per_group, 32));
+  // weight chunks must cover whole ring groups
+  while (kGatWChunk % per_group) --per_group;
+  const int smem = per_group * kHubGroups * slice_floats * 4 + kGatWChunk * a.heads * 4;
+  static bool configured = false;
+  if (!configured) {
+    GLINT_CUDA(cudaFuncSetAttribute(gat_hub_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kHubRingBytes + kGatWChunk * kMaxHeads * 4));
+    configured = true;
+  }
+  const int64_t grid = a.sc.n_hub * col_blocks;
+  gat_hub_ring_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(a, per_group,
+                                                                             slice_floats, col_blocks);
+  return launch_status("gat_aggregate_hub");
 }
 
 // Regular rows (schedule entries n_hub..n_rows), LPR lanes per row.
@@ -803,8 +1006,12 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
     if (rc) return rc;
     GLINT_CUDA(cudaEventRecord(ss->fork, s));
     GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-    gat_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
-    rc = launch_status("gat_aggregate_hub");
+    if (tuning(GLINT_TUNE_HUB_INLINE) == 1) {   // diagnostics: one-CTA-per-row register path
+      gat_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
+      rc = launch_status("gat_aggregate_hub");
+    } else {
+      rc = launch_gat_hub_ring(a, ss->stream);
+    }
     if (rc) return rc;
     GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   }
@@ -927,7 +1134,7 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
                             int64_t row_base, const int64_t* self_rows, const int32_t* col_map,
                             const float* Z, int64_t ldz, const float* s_src, const float* s_dst,
                             float slope, float* out, int64_t ld_out, const int32_t* schedule,
-                            int64_t n_hub, glint_stream_t stream) {
+                            int64_t n_hub, int32_t act, glint_stream_t stream) {
   GLINT_REQUIRE(n_rows >= 0, "gat_aggregate: n_rows must be >= 0");
   if (n_rows == 0) return GLINT_OK;
   GLINT_REQUIRE(heads >= 1 && heads <= kMaxHeads, "gat_aggregate: heads must be in [1, %d]", kMaxHeads);
@@ -951,6 +1158,8 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
   a.slope = slope;
   a.out = out;
   a.ld_out = ld_out;
+  GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "gat_aggregate: bad act %d", act);
+  a.act = act;
   const int zw = heads * head_pitch;
   a.sc.schedule = schedule;
   a.sc.n_rows = n_rows;

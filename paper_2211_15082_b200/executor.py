@@ -436,7 +436,7 @@ class LayerwiseEngine:
             if k not in ("ReLU", "LeakyReLU"):
                 continue
             x = self.m.operators[o].inputs[0]
-            if (x in blk.kinds and blk.kinds[x] in ("ConvMean", "Linear")
+            if (x in blk.kinds and blk.kinds[x] in ("ConvMean", "ConvAttn", "Linear")
                     and blk.domains[x] == "target" and blk.domains[o] == "target"
                     and self.users[x] == [o] and x not in blk.outputs):
                 fused[x] = o
@@ -787,20 +787,31 @@ class LayerwiseEngine:
                 W = op.params["weight"]
                 H, dh = int(W.shape[0]), int(W.shape[1])
                 if o not in gat_cache:
+                    if self.probe is not None:
+                        self.probe.begin("linear")
                     gat_cache[o] = kernels.attn_project(h, self.params.w_pad[o], self.params.attn[o],
                                                         H, dh, precision=self.precision)
+                    if self.probe is not None:
+                        self.probe.end(2 * int(h.shape[0]) * int(h.shape[1])
+                                       * H * kernels.head_pitch(dh))
                     self.kernel_launches += 2
                 Z, s_src, s_dst = gat_cache[o]
-                out = dest(o, H * dh)
+                act_op = fused.get(o)
+                target = act_op or o
+                out = dest(target, H * dh)
+                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
+                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
                 if self.probe is not None:
                     self.probe.begin("gat_aggregate")
                 kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, gl.indptr, gl.indices, B,
                                       row_ids=row_ids, row_base=row_base, col_map=cmap,
-                                      schedule=sched, n_hub=n_hub)
+                                      schedule=sched, n_hub=n_hub, act=act)
                 if self.probe is not None:
                     self.probe.end(agg_bytes(H * dh, plan.num_edges, B, heads=H))
                 self.kernel_launches += 1
-                mats[o] = out
+                mats[target] = out
+                if act_op is None:
+                    mats[o] = out
             else:
                 ops_, sels = zip(*(operand(p) for p in op.inputs))
                 act_op = fused.get(o)

@@ -417,11 +417,12 @@ def attn_project(h, w_pad, attn, heads, head_dim, precision=None):
 
 
 def gat_aggregate(out, Z, s_src, s_dst, heads, head_dim, indptr, indices, n_rows, row_ids=None,
-                  row_base=0, self_rows=None, col_map=None, schedule=None, n_hub=0):
+                  row_base=0, self_rows=None, col_map=None, schedule=None, n_hub=0,
+                  act=0):
     _lib.call("glint_gat_aggregate_f32", int(n_rows), heads, head_dim, head_pitch(head_dim),
               ptr(indptr), ptr(indices), ptr(row_ids), int(row_base), ptr(self_rows),
               ptr(col_map), ptr(Z), ld(Z), ptr(s_src), ptr(s_dst), float(LEAKY_SLOPE), ptr(out),
-              ld(out), ptr(schedule), int(n_hub), stream_handle())
+              ld(out), ptr(schedule), int(n_hub), int(act), stream_handle())
     return out
 
 

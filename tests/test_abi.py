@@ -40,7 +40,7 @@ def test_argument_errors_map_to_value_error_without_gpu():
         _lib.call("glint_elementwise_f32", 99, 1, 1, 1, None, None, None, None, 1, None)
     with pytest.raises(ValueError, match="heads"):
         _lib.call("glint_gat_aggregate_f32", 1, 9, 4, 4, None, None, None, 0, None, None, None, 4,
-                  None, None, 0.2, None, 4, None, 0, None)
+                  None, None, 0.2, None, 4, None, 0, 0, None)
     assert "heads" in _lib.last_error()
 
 

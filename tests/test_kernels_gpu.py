@@ -187,6 +187,43 @@ def test_agg_attn_hubs_and_widths(cuda, heads, dh):
     assert rel_l2(got, want) <= 1e-5
 
 
+@pytest.mark.parametrize("heads,dh", [(4, 64), (4, 47), (3, 5)])
+def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
+    """Hub rows: bulk-copy ring kernel == one-CTA register path, byte for byte
+    (same per-column order); the fused ReLU epilogue == ReLU of the output."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(dh)
+    n = 3000
+    degs = rng.integers(0, 40, size=n)
+    degs[[5, 1200, 2999]] = [4500, 700, 2048]
+    indptr = torch.from_numpy(np.concatenate([[0], np.cumsum(degs)]).astype(np.int64)).cuda()
+    indices = torch.from_numpy(rng.integers(0, n, size=int(degs.sum())).astype(np.int32)).cuda()
+    hp = kernels.head_pitch(dh)
+    Z = torch.randn((n, heads * hp), device="cuda")
+    Z.view(n, heads, hp)[:, :, dh:] = 0
+    s_src = torch.randn((n, heads), device="cuda")
+    s_dst = torch.randn((n, heads), device="cuda")
+    sched, nh = kernels.degree_schedule(indptr, None, 0, n)
+    outs = []
+    for inline, act in ((0, 0), (1, 0), (0, 1)):
+        _lib.call("glint_set_tuning", 2, inline)
+        out = torch.empty((n, heads * dh), device="cuda")
+        kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, indptr, indices, n,
+                              schedule=sched, n_hub=int(nh.item()), act=act)
+        outs.append(out)
+    _lib.call("glint_set_tuning", 2, 0)
+    assert int(nh.item()) == 3
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(torch.relu(outs[0]), outs[2])
+    # and the same bytes without any hub path (every row in the regular kernel)
+    plain = torch.empty_like(outs[0])
+    kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n)
+    assert torch.equal(plain, outs[0])
+
+
 def test_attn_zero_logits_equal_mean_after_transform(cuda):
     """Reference test_kernels.py:101-109 (tolerance: the transform is a GEMM)."""
     from paper_2211_15082_b200 import kernels
