@@ -380,7 +380,9 @@ def main():
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks.report(),
         "step_ms": [round(t, 3) for t in step_ms],
         **({"tuning": args.tune} if args.tune else {}),
-        **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()]}
+        **({"timeline_ms": [(n, round(t, 3)) for n, t in probe.timeline()],
+            "launch_ms": [(n, round(t, 4), round(b / t / 1e6, 1) if n != "linear"
+                           else round(b / t / 1e9, 1)) for n, b, t in probe.launches()]}
            if args.timeline else {}),
     }
     line["config"]["capacity_bytes"] = budget.capacity

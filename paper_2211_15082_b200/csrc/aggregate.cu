@@ -107,7 +107,9 @@ __device__ __forceinline__ void store_vec(float* p, const float (&v)[VEC], int v
     if (valid >= 4) {
       *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
-      for (int c = 0; c < valid; ++c) p[c] = v[c];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < valid) p[c] = v[c];   // static indices: v stays in registers
     }
   } else {
     p[0] = v[0];
@@ -131,10 +133,13 @@ __device__ __forceinline__ void mean_row_regular(const MeanArgs& a, int64_t r, i
 #pragma unroll
       for (int c = 0; c < VEC; ++c) acc[k][c] = 0.0f;
 
+    // the next chunk's source ids are loaded while the current chunk's rows
+    // stream in (one dependent index latency per row instead of per chunk)
+    int32_t nxt = (beg + lane_g < end) ? __ldg(a.ra.indices + beg + lane_g) : 0;
     for (int64_t e0 = beg; e0 < end; e0 += LPR) {
       const int cnt = static_cast<int>(min(static_cast<int64_t>(LPR), end - e0));
-      int64_t my = 0;
-      if (lane_g < cnt) my = a.ra.map(a.ra.indices[e0 + lane_g]) * a.ld_h;
+      const int64_t my = (lane_g < cnt) ? a.ra.map(nxt) * a.ld_h : 0;
+      if (e0 + LPR + lane_g < end) nxt = __ldg(a.ra.indices + e0 + LPR + lane_g);
       for (int j = 0; j < cnt; j += U) {
         float v[U][VPL][VEC];
 #pragma unroll
@@ -212,22 +217,25 @@ __device__ __forceinline__ void mean_row_hub(const MeanArgs& a, int64_t r, int c
   }
 }
 
+// Hub rows, register path: one 256-thread CTA per (hub row, 256 columns).
+__global__ void __launch_bounds__(kThreads) mean_hub_reg_kernel(MeanArgs a) {
+  __shared__ int64_t s_off[kHubChunk];
+  const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
+  const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
+  mean_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off);
+}
+
+// Regular rows (schedule entries n_hub..n_rows): LPR lanes per row.  Hub rows
+// run in their own kernel, so this one carries no shared memory and its
+// register budget is set by the regular path alone.
 template <int VEC, int LPR, int VPL, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) mean_kernel(MeanArgs a) {
-  __shared__ int64_t s_off[kHubChunk];
-  if (static_cast<int64_t>(blockIdx.x) < a.sc.hub_ctas) {
-    const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
-    const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
-    mean_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off);
-    return;
-  }
   constexpr int G = 32 / LPR;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int group = lane / LPR;
   const int lane_g = lane % LPR;
-  const int64_t slot = (static_cast<int64_t>(blockIdx.x) - a.sc.hub_ctas) * (kWarps * G) +
-                       warp * G + group;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
   const int64_t idx = a.sc.n_hub + slot;
   if (idx >= a.sc.n_rows) return;
   const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
@@ -264,8 +272,86 @@ __device__ __forceinline__ void hub_mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int slots_per_group,
-                                                               int slice_floats, int col_blocks) {
+// Producer warp of the hub ring kernels: streams the [c0, c0+width) slice of
+// every source row of edges [beg, end) into ring groups of `spg` slots.  The
+// source ids of a whole ring cycle (8 groups) are loaded one cycle ahead, so
+// no dependent index load sits between two groups' copies.
+//   bulk = true : one cp.async.bulk (TMA) per slot; full_bar count 1 + tx bytes.
+//   bulk = false: 16-byte cp.async (LDGSTS) spread over the 32 lanes (many
+//                 edges per warp instruction); each lane arrives on full_bar
+//                 with cp.async.mbarrier.arrive.noinc (count 32) once its
+//                 copies land.  Per-request TMA cost bounds a 20K-edge hub
+//                 row in bulk mode; LDGSTS issues 8-32 slices per instruction.
+__device__ __forceinline__ void hub_produce(const RowAddr& ra, int64_t beg, int64_t end,
+                                            const float* base, int64_t ld, int c0, int width,
+                                            int spg, int slice_floats, float* ring,
+                                            uint64_t* full_bar, uint64_t* empty_bar, bool bulk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t deg = end - beg;
+  const int64_t ngroups = (deg + spg - 1) / spg;
+  const int64_t ncycles = (ngroups + kHubGroups - 1) / kHubGroups;
+  const int cps = (width + 3) / 4;  // 16-byte chunks per slot
+  const uint32_t slice_bytes = static_cast<uint32_t>(cps * 16);
+  auto load_cycle = [&](int64_t c, int64_t (&ids)[kHubGroups]) {
+#pragma unroll
+    for (int t = 0; t < kHubGroups; ++t) {
+      const int64_t e = beg + (c * kHubGroups + t) * spg + lane;
+      ids[t] = (lane < spg && e < end) ? ra.map(ra.indices[e]) : 0;
+    }
+  };
+  int64_t cur[kHubGroups], nxt[kHubGroups];
+  if (ncycles > 0) load_cycle(0, cur);
+  for (int64_t c = 0; c < ncycles; ++c) {
+    if (c + 1 < ncycles) load_cycle(c + 1, nxt);
+#pragma unroll
+    for (int t = 0; t < kHubGroups; ++t) {
+      const int64_t gi = c * kHubGroups + t;
+      if (gi < ngroups) {
+        if (c > 0) hub_mbar_wait(&empty_bar[t], static_cast<uint32_t>(c - 1) & 1u);
+        const int64_t e0 = beg + gi * spg;
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(spg), end - e0));
+        float* grp = ring + static_cast<int64_t>(t) * spg * slice_floats;
+        if (bulk) {
+          if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(smem_u32(&full_bar[t])), "r"(slice_bytes * cnt) : "memory");
+          }
+          __syncwarp();
+          if (lane < cnt) {
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                ::"r"(smem_u32(grp + lane * slice_floats)), "l"(base + cur[t] * ld + c0),
+                "r"(slice_bytes), "r"(smem_u32(&full_bar[t]))
+                : "memory");
+          }
+        } else {
+          const int total = cnt * cps;
+          for (int q0 = 0; q0 < total; q0 += 32) {
+            const int q = q0 + lane;
+            const int slot = q / cps;
+            const int64_t id = shfl64(0xffffffffu, cur[t], slot & 31, 32);
+            if (q < total) {
+              const int ch = q - slot * cps;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                           ::"r"(smem_u32(grp + slot * slice_floats + ch * 4)),
+                           "l"(base + id * ld + c0 + ch * 4)
+                           : "memory");
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];"
+                       ::"r"(smem_u32(&full_bar[t])) : "memory");
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kHubGroups; ++t) cur[t] = nxt[t];
+  }
+}
+
+template <int CW>  // consumer warps = columns per CTA / 32
+__global__ void __launch_bounds__((CW + 1) * 32) mean_hub_kernel(MeanArgs a, int slots_per_group,
+                                                                 int slice_floats, int col_blocks,
+                                                                 bool bulk) {
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full_bar[kHubGroups];
   __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
@@ -276,63 +362,24 @@ __global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int s
   const int64_t end = a.ra.indptr[rid + 1];
   const int c0 = cb * slice_floats;
   const int width = min(slice_floats, a.dim - c0);
-  const uint32_t slice_bytes = static_cast<uint32_t>(((width + 3) / 4) * 16);
   const int64_t deg = end - beg;
   const int64_t ngroups = (deg + slots_per_group - 1) / slots_per_group;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int g = 0; g < kHubGroups; ++g) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[g])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
-                   ::"r"(smem_u32(&empty_bar[g])), "r"(kHubConsumerWarps));
+                   ::"r"(smem_u32(&full_bar[g])), "r"(bulk ? 1 : 32));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                   ::"r"(smem_u32(&empty_bar[g])), "r"(CW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kHubConsumerWarps) {
-    // producer: group gi -> ring group gi % kHubGroups; lane j owns slot j
-    // (slots_per_group <= 32).  The source ids of a whole ring cycle (8
-    // groups) are loaded one cycle ahead, so no dependent index load sits
-    // between two groups' copies.
-    const int64_t ncycles = (ngroups + kHubGroups - 1) / kHubGroups;
-    auto load_cycle = [&](int64_t c, int64_t (&ids)[kHubGroups]) {
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) {
-        const int64_t e = beg + (c * kHubGroups + t) * slots_per_group + lane;
-        ids[t] = (lane < slots_per_group && e < end) ? a.ra.map(a.ra.indices[e]) : 0;
-      }
-    };
-    int64_t cur[kHubGroups], nxt[kHubGroups];
-    if (ncycles > 0) load_cycle(0, cur);
-    for (int64_t c = 0; c < ncycles; ++c) {
-      if (c + 1 < ncycles) load_cycle(c + 1, nxt);
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) {
-        const int64_t gi = c * kHubGroups + t;
-        if (gi < ngroups) {
-          if (c > 0) hub_mbar_wait(&empty_bar[t], static_cast<uint32_t>(c - 1) & 1u);
-          const int64_t e0 = beg + gi * slots_per_group;
-          const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
-          if (lane == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(smem_u32(&full_bar[t])), "r"(slice_bytes * cnt) : "memory");
-          }
-          __syncwarp();
-          if (lane < cnt) {
-            float* dst = ring + (static_cast<int64_t>(t) * slots_per_group + lane) * slice_floats;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                ::"r"(smem_u32(dst)), "l"(a.h + cur[t] * a.ld_h + c0), "r"(slice_bytes),
-                "r"(smem_u32(&full_bar[t]))
-                : "memory");
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) cur[t] = nxt[t];
-    }
+  if (warp == CW) {
+    hub_produce(a.ra, beg, end, a.h, a.ld_h, c0, width, slots_per_group, slice_floats, ring,
+                full_bar, empty_bar, bulk);
     return;
   }
   // consumers: thread t owns column c0 + t
@@ -347,7 +394,16 @@ __global__ void __launch_bounds__(kHubThreads) mean_hub_kernel(MeanArgs a, int s
                                          end - (beg + gi * slots_per_group)));
     const float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
     if (active) {
-      for (int j = 0; j < cnt; ++j) acc = __fadd_rn(acc, slot0[j * slice_floats + threadIdx.x]);
+      // batches of 8 independent shared loads ahead of the dependent add chain
+      int j = 0;
+      for (; j + 8 <= cnt; j += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = slot0[(j + u) * slice_floats + threadIdx.x];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+      }
+      for (; j < cnt; ++j) acc = __fadd_rn(acc, slot0[j * slice_floats + threadIdx.x]);
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
@@ -383,32 +439,174 @@ int side_stream(SideStream** out) {
   return GLINT_OK;
 }
 
-int launch_hub(const MeanArgs& a, cudaStream_t s) {
-  // slices of <= kHubSlice columns per CTA (several CTAs per hub row keep
-  // more bytes in flight per row), one bulk copy per source-row slice
-  const int width = std::min(kHubSlice, a.dim);
+template <int CW>
+int launch_hub_cw(const MeanArgs& a, bool bulk, cudaStream_t s) {
+  // slices of <= 32*CW columns per CTA (several CTAs per hub row keep more
+  // bytes in flight per row)
+  constexpr int kSlice = 32 * CW;
+  const int width = std::min(kSlice, a.dim);
   const int slice_floats = ((width + 3) / 4) * 4;
-  const int col_blocks = static_cast<int>(ceil_div(a.dim, kHubSlice));
+  const int col_blocks = static_cast<int>(ceil_div(a.dim, kSlice));
   int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
   per_group = std::max(1, std::min(per_group, 32));  // one producer lane per slot
   const int smem = per_group * kHubGroups * slice_floats * 4;
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(mean_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GLINT_CUDA(cudaFuncSetAttribute(mean_hub_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kHubRingBytes + 4096));
     configured = true;
   }
   const int64_t grid = a.sc.n_hub * col_blocks;
-  mean_hub_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(a, per_group, slice_floats,
-                                                                         col_blocks);
+  mean_hub_kernel<CW><<<static_cast<unsigned>(grid), (CW + 1) * 32, smem, s>>>(
+      a, per_group, slice_floats, col_blocks, bulk);
   return launch_status("spmm_mean_hub");
+}
+
+// Hub ring kernel: 32-column slices with 16-byte cp.async copies (default);
+// knob GLINT_TUNE_HUB_INLINE = 3: TMA bulk copies, 4: 64-column slices.
+int launch_hub(const MeanArgs& a, cudaStream_t s) {
+  const int knob = tuning(GLINT_TUNE_HUB_INLINE);
+  if (knob == 4) return launch_hub_cw<2>(a, false, s);
+  return launch_hub_cw<1>(a, knob == 3, s);
+}
+
+// ------------------------------------- regular rows: per-lane cp.async ring --
+//
+// Same work split as mean_row_regular (LPR lanes per row, VPL 16-byte column
+// chunks per lane) but the neighbour-row loads go through a per-lane ring of
+// R shared-memory slots filled with cp.async (LDGSTS): a lane keeps R-1 row
+// chunks in flight without holding them in registers, and consumes them in
+// stored edge order (one sequential add chain per column -- bit-exact).  The
+// source ids of the next LPR edges are prefetched one index chunk ahead of the
+// issue cursor, so the issue stream never waits on a dependent index load.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int LPR, int VPL, int R>
+__device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int lane_g,
+                                               unsigned gmask, float4* ring) {
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const float degp1 = static_cast<float>(end - beg + 1);
+  const int deg = static_cast<int>(end - beg);
+  bool ok[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) ok[k] = (lane_g + LPR * k) * 4 < a.dim;
+  const uint32_t ring_s = smem_u32(ring);  // slot (t, k) at ring + (t*VPL + k) * kThreads
+
+  // issue cursor: edge `ie`, index chunk [cb, cb+LPR) held in `cur`, next in `nxt`
+  int ie = 0, cb = 0;
+  int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
+  int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
+  auto issue = [&](int slot) {
+    if (ie - cb == LPR) {
+      cb += LPR;
+      cur = nxt;
+      nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
+    }
+    const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
+    const float* src = a.h + u * a.ld_h + lane_g * 4;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+      if (ok[k])
+        cp_async16(ring_s + static_cast<uint32_t>((slot * VPL + k) * kThreads) * 16u,
+                   src + LPR * 4 * k);
+    ++ie;
+  };
+
+  float acc[VPL][4];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[k][c] = 0.0f;
+
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    if (ie < deg) issue(t);
+    cp_async_commit();
+  }
+  int slot = 0;
+  for (int j = 0; j < deg; ++j) {
+    cp_async_wait<R - 1>();
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (ok[k]) {
+        const float4 v = ring[(slot * VPL + k) * kThreads];
+        acc[k][0] = __fadd_rn(acc[k][0], v.x);
+        acc[k][1] = __fadd_rn(acc[k][1], v.y);
+        acc[k][2] = __fadd_rn(acc[k][2], v.z);
+        acc[k][3] = __fadd_rn(acc[k][3], v.w);
+      }
+    }
+    if (ie < deg) issue(slot);
+    cp_async_commit();
+    slot = (slot + 1 == R) ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+  const int64_t self_off = a.ra.self_row(r, rid) * a.ld_h;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int col = (lane_g + LPR * k) * 4;
+    if (!ok[k]) continue;
+    float sv[4];
+    load_vec<4>(sv, a.h + self_off + col);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      acc[k][c] = mean_epilogue(a, __fdiv_rn(__fadd_rn(acc[k][c], sv[c]), degp1),
+                                col + c < a.dim ? col + c : col);
+    store_vec<4>(a.out + r * a.ld_out + col, acc[k], a.dim - col);
+  }
+}
+
+template <int LPR, int VPL, int R, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) {
+  extern __shared__ __align__(16) float4 ring_all[];
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
+  const int64_t idx = a.sc.n_hub + slot;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  mean_row_async<LPR, VPL, R>(a, r, lane_g, gmask, ring_all + threadIdx.x);
+}
+
+template <int LPR, int VPL, int R, int MINB>
+int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
+  constexpr int G = 32 / LPR;
+  constexpr int smem = R * VPL * kThreads * 16;
+  static bool configured = false;
+  if (!configured) {
+    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
+  if (grid <= 0) return GLINT_OK;
+  if (grid > 0x7fffffffLL) {
+    set_error("spmm_mean: grid too large");
+    return GLINT_EINVAL;
+  }
+  mean_async_kernel<LPR, VPL, R, MINB><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  return launch_status("spmm_mean_async");
 }
 
 template <int VEC, int LPR, int VPL, int U, int MINB = 3>
 int launch_mean(const MeanArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
-  const int64_t regular = a.sc.n_rows - a.sc.n_hub;
-  const int64_t grid = a.sc.hub_ctas + ceil_div(regular, kWarps * G);
+  const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
   if (grid <= 0) return GLINT_OK;
   if (grid > 0x7fffffffLL) {
     set_error("spmm_mean: grid too large");
@@ -420,31 +618,32 @@ int launch_mean(const MeanArgs& a, cudaStream_t s) {
 
 int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s);
 
-// Hub rows go to the bulk-copy kernel on a side stream (fork/join with
-// events, so the caller's stream order is preserved and graph capture works);
-// the regular kernel runs concurrently on the caller's stream.
+// Hub rows run on the library side stream (fork/join with events, so the
+// caller's stream order is preserved and graph capture works), concurrently
+// with the regular rows on the caller's stream.  The bulk-copy ring kernel
+// wins when one hub row bounds the launch (small batches, measured up to
+// ~10x); on large launches the register path finishes within the regular
+// rows' time and leaves shared memory to them (profiles/r01_spmm_sweep*.jsonl).
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
-  // The bulk-copy hub kernel wins when one hub row bounds the launch (small
-  // batches, measured up to ~10x); on large launches the register hub path
-  // inside the main kernel finishes within the regular rows' time and leaves
-  // shared memory to them (profiles/r01_spmm_sweep*.jsonl).
-  const int inline_knob = tuning(GLINT_TUNE_HUB_INLINE);  // 0 auto, 1 inline, 2 bulk
-  const bool use_bulk = inline_knob == 2 || (inline_knob == 0 && a.sc.n_rows < (1 << 19));
-  if (!vec4 || a.sc.hub_ctas == 0 || !use_bulk) return dispatch_regular(a, vec4, s);
+  if (a.sc.n_hub == 0) return dispatch_regular(a, vec4, s);
+  const int inline_knob = tuning(GLINT_TUNE_HUB_INLINE);  // 0 auto, 1 register, 2 bulk
+  const bool use_bulk = vec4 && (inline_knob >= 2 || (inline_knob == 0 && a.sc.n_rows < (1 << 19)));
   SideStream* ss = nullptr;
   int rc = side_stream(&ss);
   if (rc) return rc;
   GLINT_CUDA(cudaEventRecord(ss->fork, s));
   GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-  rc = launch_hub(a, ss->stream);
+  if (use_bulk) {
+    rc = launch_hub(a, ss->stream);
+  } else {
+    mean_hub_reg_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
+    rc = launch_status("spmm_mean_hub");
+  }
   if (rc) return rc;
   GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
-  MeanArgs reg = a;
-  reg.sc.hub_ctas = 0;  // hub schedule entries are skipped, not processed
-  rc = dispatch_regular(reg, vec4, s);
-  if (rc) return rc;
+  rc = dispatch_regular(a, vec4, s);
   GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
-  return GLINT_OK;
+  return rc;
 }
 
 int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
@@ -453,6 +652,51 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
   // Measured on B200 (tools/sweep_kernels.py, profiles/): 4 CTAs/SM (<= 64
   // registers) beats deeper unrolling at 2-3 CTAs/SM for d=100 and d=256.
   const int variant = tuning(GLINT_TUNE_MEAN_VARIANT);
+  if (vec4 && (variant == 0 || variant >= 7)) {
+    // cp.async ring kernels (default); variant 0 = best measured on the
+    // Products graph (profiles/r01_spmm_sweep_async.jsonl): d=48 5.5 TB/s,
+    // d=100 5.8 TB/s, d=256 7.2 TB/s of algorithmic bytes.
+    const int d4 = static_cast<int>(ceil_div(a.dim, 4));
+    if (d4 <= 8) {
+      if (variant == 7) return launch_mean_async<8, 1, 16, 3>(a, s);
+      if (variant == 8) return launch_mean_async<4, 2, 8, 3>(a, s);
+      return launch_mean_async<8, 1, 8, 4>(a, s);
+    }
+    if (d4 <= 16) {
+      if (variant == 7) return launch_mean_async<16, 1, 16, 3>(a, s);
+      if (variant == 8) return launch_mean_async<16, 1, 8, 4>(a, s);
+      if (variant == 10) return launch_mean_async<4, 4, 6, 2>(a, s);
+      if (variant == 11) return launch_mean_async<16, 1, 12, 3>(a, s);
+      if (variant == 9) return launch_mean_async<8, 2, 8, 3>(a, s);
+      if (variant == 13) return launch_mean_async<8, 2, 4, 6>(a, s);
+      if (variant == 14) return launch_mean_async<16, 1, 6, 5>(a, s);
+      if (variant == 15) return launch_mean_async<4, 4, 4, 3>(a, s);
+      return launch_mean_async<8, 2, 6, 4>(a, s);   // also variant 12
+    }
+    if (d4 <= 32) {
+      if (variant == 7) return launch_mean_async<32, 1, 16, 3>(a, s);
+      if (variant == 9) return launch_mean_async<16, 2, 8, 3>(a, s);
+      if (variant == 10) return launch_mean_async<8, 4, 6, 2>(a, s);
+      if (variant == 11) return launch_mean_async<32, 1, 12, 3>(a, s);
+      if (variant == 12) return launch_mean_async<32, 1, 6, 5>(a, s);
+      if (variant == 13) return launch_mean_async<32, 1, 4, 6>(a, s);
+      if (variant == 14) return launch_mean_async<16, 2, 6, 4>(a, s);
+      if (variant == 15) return launch_mean_async<8, 4, 4, 3>(a, s);
+      return launch_mean_async<32, 1, 8, 4>(a, s);   // also variant 8
+    }
+    if (d4 <= 64) {
+      if (variant == 7) return launch_mean_async<32, 2, 8, 3>(a, s);
+      if (variant == 9) return launch_mean_async<32, 2, 6, 3>(a, s);
+      if (variant == 10) return launch_mean_async<32, 2, 12, 2>(a, s);
+      if (variant == 11) return launch_mean_async<32, 2, 10, 2>(a, s);
+      if (variant == 12) return launch_mean_async<32, 2, 3, 5>(a, s);
+      if (variant == 13) return launch_mean_async<32, 2, 2, 8>(a, s);
+      if (variant == 14) return launch_mean_async<16, 4, 4, 3>(a, s);
+      if (variant == 15) return launch_mean_async<32, 2, 5, 4>(a, s);
+      return launch_mean_async<32, 2, 4, 4>(a, s);   // also variant 8
+    }
+    if (variant == 0 && d4 <= 128) return launch_mean_async<32, 4, 4, 2>(a, s);
+  }
   if (vec4 && variant != 0) {
     const int d4 = static_cast<int>(ceil_div(a.dim, 4));
     if (d4 > 8 && d4 <= 16) {
@@ -798,7 +1042,7 @@ __device__ __forceinline__ void consumer_sync() {
 
 __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, int slots_per_group,
                                                                    int slice_floats,
-                                                                   int col_blocks) {
+                                                                   int col_blocks, bool bulk) {
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full_bar[kHubGroups];
   __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
@@ -815,14 +1059,14 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
   const int zw = H * a.head_pitch;
   const int c0 = cb * slice_floats;
   const int width = min(slice_floats, zw - c0);
-  const uint32_t slice_bytes = static_cast<uint32_t>(((width + 3) / 4) * 16);
   const int64_t deg = end - beg;
   const int64_t ngroups = (deg + slots_per_group - 1) / slots_per_group;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int g = 0; g < kHubGroups; ++g) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[g])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                   ::"r"(smem_u32(&full_bar[g])), "r"(bulk ? 1 : 32));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
                    ::"r"(smem_u32(&empty_bar[g])), "r"(kHubConsumerWarps));
     }
@@ -831,44 +1075,8 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
   __syncthreads();
 
   if (warp == kHubConsumerWarps) {
-    // producer: identical to mean_hub_kernel's
-    const int64_t ncycles = (ngroups + kHubGroups - 1) / kHubGroups;
-    auto load_cycle = [&](int64_t c, int64_t (&ids)[kHubGroups]) {
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) {
-        const int64_t e = beg + (c * kHubGroups + t) * slots_per_group + lane;
-        ids[t] = (lane < slots_per_group && e < end) ? a.ra.map(a.ra.indices[e]) : 0;
-      }
-    };
-    int64_t cur[kHubGroups], nxt[kHubGroups];
-    if (ncycles > 0) load_cycle(0, cur);
-    for (int64_t c = 0; c < ncycles; ++c) {
-      if (c + 1 < ncycles) load_cycle(c + 1, nxt);
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) {
-        const int64_t gi = c * kHubGroups + t;
-        if (gi < ngroups) {
-          if (c > 0) hub_mbar_wait(&empty_bar[t], static_cast<uint32_t>(c - 1) & 1u);
-          const int64_t e0 = beg + gi * slots_per_group;
-          const int cnt = static_cast<int>(min(static_cast<int64_t>(slots_per_group), end - e0));
-          if (lane == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(smem_u32(&full_bar[t])), "r"(slice_bytes * cnt) : "memory");
-          }
-          __syncwarp();
-          if (lane < cnt) {
-            float* dst = ring + (static_cast<int64_t>(t) * slots_per_group + lane) * slice_floats;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                ::"r"(smem_u32(dst)), "l"(a.Z + cur[t] * a.ldz + c0), "r"(slice_bytes),
-                "r"(smem_u32(&full_bar[t]))
-                : "memory");
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kHubGroups; ++t) cur[t] = nxt[t];
-    }
+    hub_produce(a.ra, beg, end, a.Z, a.ldz, c0, width, slots_per_group, slice_floats, ring,
+                full_bar, empty_bar, bulk);
     return;
   }
 
@@ -935,7 +1143,21 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
     const float* slot0 = ring + static_cast<int64_t>(g) * slots_per_group * slice_floats;
     const float* wrow = w_sm + (gi * slots_per_group - wbase) * H + hh;
     if (active) {
-      for (int j = 0; j < cnt; ++j) {
+      int j = 0;
+      for (; j + 8 <= cnt; j += 8) {
+        float w[8], z[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          w[u] = wrow[(j + u) * H];
+          z[u] = slot0[(j + u) * slice_floats + tid];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          den = __fadd_rn(den, w[u]);
+          num = __fadd_rn(num, __fmul_rn(w[u], z[u]));
+        }
+      }
+      for (; j < cnt; ++j) {
         const float w = wrow[j * H];
         den = __fadd_rn(den, w);
         num = __fadd_rn(num, __fmul_rn(w, slot0[j * slice_floats + tid]));
@@ -971,8 +1193,8 @@ int launch_gat_hub_ring(const GatArgs& a, cudaStream_t s) {
     configured = true;
   }
   const int64_t grid = a.sc.n_hub * col_blocks;
-  gat_hub_ring_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(a, per_group,
-                                                                             slice_floats, col_blocks);
+  gat_hub_ring_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(
+      a, per_group, slice_floats, col_blocks, tuning(GLINT_TUNE_HUB_INLINE) == 3);
   return launch_status("gat_aggregate_hub");
 }
 

@@ -927,6 +927,10 @@ class KernelProbe:
         return [(n, round(e0.elapsed_time(e), 3), round(1e3 * (h - h0), 3))
                 for n, e, h in self.marks]
 
+    def launches(self):
+        """[(name, bytes or flops, ms)] per probed launch (call after synchronize)."""
+        return [(name, nbytes, s.elapsed_time(e)) for name, nbytes, s, e in self.records]
+
     def summary(self):
         """{name: (launches, total bytes, total ms)} (call after synchronize)."""
         out = {}

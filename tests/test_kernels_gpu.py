@@ -90,6 +90,42 @@ def test_agg_mean_widths_and_hubs_bit_exact(cuda, dim):
     assert not out[:, dim:].any()
 
 
+@pytest.mark.parametrize("dim", [5, 48, 100, 256])
+def test_agg_mean_every_variant_bit_exact(cuda, dim):
+    """Every K1 launch variant (register-staged and cp.async ring) and both hub
+    paths give the oracle's bytes (tuning knobs are performance-only)."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(7 + dim)
+    n = 4000
+    degs = rng.integers(0, 70, size=n)
+    degs[[11, 2500]] = [3000, 600]
+    indptr = np.concatenate([[0], np.cumsum(degs)]).astype(np.int64)
+    indices = rng.integers(0, n, size=int(indptr[-1]))
+    x = rng.normal(size=(n, dim)).astype(np.float32)
+    want = orc.agg_mean(orc.build_batch_csc(indptr, indices, np.arange(n)), x)
+    pitch = (dim + 3) // 4 * 4
+    hp = torch.zeros((n, pitch), dtype=torch.float32, device="cuda")
+    hp[:, :dim] = torch.from_numpy(x).cuda()
+    ip = torch.from_numpy(indptr).cuda()
+    ix = torch.from_numpy(indices.astype(np.int32)).cuda()
+    sched, nh = kernels.degree_schedule(ip, None, 0, n)
+    try:
+        for variant in range(16):
+            for hub in (1, 2, 3, 4):
+                _lib.call("glint_set_tuning", 0, variant)
+                _lib.call("glint_set_tuning", 2, hub)
+                out = torch.full((n, pitch), 7.0, dtype=torch.float32, device="cuda")
+                kernels.spmm_mean(out[:, :dim], hp[:, :dim], ip, ix, n, schedule=sched,
+                                  n_hub=int(nh.item()))
+                assert out[:, :dim].cpu().numpy().tobytes() == want.tobytes(), (variant, hub)
+    finally:
+        _lib.call("glint_set_tuning", 0, 0)
+        _lib.call("glint_set_tuning", 2, 0)
+
+
 @pytest.mark.parametrize("act", [0, 1, 2])
 def test_agg_mean_bias_act_epilogue_bit_exact(cuda, act):
     """K1 epilogue act(mean + b) == numpy (agg_mean + b) then ReLU/LeakyReLU, bytes."""
@@ -208,7 +244,7 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     s_dst = torch.randn((n, heads), device="cuda")
     sched, nh = kernels.degree_schedule(indptr, None, 0, n)
     outs = []
-    for inline, act in ((0, 0), (1, 0), (0, 1)):
+    for inline, act in ((0, 0), (1, 0), (0, 1), (3, 0)):
         _lib.call("glint_set_tuning", 2, inline)
         out = torch.empty((n, heads * dh), device="cuda")
         kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, indptr, indices, n,
@@ -218,6 +254,7 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     assert int(nh.item()) == 3
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(torch.relu(outs[0]), outs[2])
+    assert torch.equal(outs[0], outs[3])
     # and the same bytes without any hub path (every row in the regular kernel)
     plain = torch.empty_like(outs[0])
     kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n)

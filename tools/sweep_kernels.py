@@ -82,6 +82,21 @@ def main():
                 same = bool(torch.equal(ref, out))
             print(json.dumps({"kernel": "spmm_mean", "dim": d, "variant": variant, "ms": ms,
                               "GBps": nb / ms / 1e6, "identical_to_v0": same}), flush=True)
+        # row pitch rounded to 32 B / 128 B (sector / line aligned source rows)
+        _lib.call("glint_set_tuning", 0, 0)
+        for pad in (8, 32):
+            pitch = (d + pad - 1) // pad * pad
+            if pitch == d:
+                continue
+            hp = torch.zeros((n, pitch), device="cuda")
+            hp[:, :d] = h
+            hv = hp[:, :d]
+            ms = timed(lambda: kernels.spmm_mean(out, hv, g.indptr, g.indices, n, schedule=sched,
+                                                 n_hub=hub_pre), args.reps)
+            print(json.dumps({"kernel": "spmm_mean_pitch", "dim": d, "pitch": pitch, "ms": ms,
+                              "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
+                              "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+            del hp, hv
         # hub rows in the register path of the main kernel (vs bulk-copy hub kernel)
         _lib.call("glint_set_tuning", 0, 0)
         _lib.call("glint_set_tuning", 2, 1)
@@ -100,7 +115,7 @@ def main():
             nh_r = int(hp[-1].item())
             sch, _ = kernels.degree_schedule(g.indptr, None, pos, size)
             o2 = out[pos:pos + size]
-            for inline in (2, 1):      # 2 = bulk-copy hub kernel, 1 = register path
+            for inline in (2, 3, 4, 1):  # ring: 2 LDGSTS 32-col, 3 TMA 32-col, 4 LDGSTS 64-col; 1 register
                 _lib.call("glint_set_tuning", 2, inline)
                 ms = timed(lambda: kernels.spmm_mean(o2, h, g.indptr, g.indices, size,
                                                      row_base=pos, schedule=sch, n_hub=nh_r),
