@@ -146,6 +146,8 @@ struct TcArgs {
   int n_tiles;
   int nkb;
   bool c_vec4;
+  bool raw_hi;               // experiment knob GLINT_TUNE_GEMM_RAWHI (v1 kernel only)
+  bool mma_only;             // diagnostics knob GLINT_TUNE_GEMM_PROF == 2 (v2 kernel)
   unsigned long long* prof;  // optional phase-cycle counters (GLINT_TUNE_GEMM_PROF)
 };
 
@@ -291,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
         const int r = (wq + 4 * i) * 8 + rsub;
         const uint32_t off = (r >= HALF ? C::A_BYTES / 2 : 0) + tile_off(r & (HALF - 1), chunk);
         split_store(a_hi, a_lo, off, va[i]);
+        if (a.raw_hi)  // experiment: feed the unmasked fp32 as the "hi" operand
+          *reinterpret_cast<float4*>(a_hi + off) = va[i];
       }
 #pragma unroll
       for (int i = 0; i < WG; ++i) {
@@ -482,6 +486,405 @@ int launch_bn(const TcArgs& a, int act, cudaStream_t s) {
   return launch_act<256, VEC>(a, act, s);
 }
 
+// ============================================================== v2 kernel --
+//
+// Same split-TF32 products and k order as the kernel above, restructured for
+// the two limits measured on it (phase counters, ncu source stalls): the
+// producers stalled on A's DRAM latency with only ~1 stage of lookahead, and
+// the epilogue serialised with the MMAs.
+//   * The tensor core truncates fp32 operands of kind::tf32 to TF32 (ignores
+//     the low 13 mantissa bits; verified bit-for-bit, tools/tf32_trunc_probe.py),
+//     so the raw fp32 A tile IS the "hi" operand: producers cp.async (LDGSTS)
+//     raw A rows straight into the canonical K-major UMMA layout RA-1 k-steps
+//     ahead (no registers held), then compute only lo = a - trunc(a) into a
+//     small lo ring just before the MMA needs it.
+//   * W is pre-split once per call (w_panel_kernel) into hi/lo blocks already in
+//     the UMMA layout; a loader warp streams one block per k-step with ONE
+//     cp.async.bulk (TMA engine, mbarrier tx-count), RW steps ahead.
+//   * Tiles are 256 rows x BN <= 128 columns; TMEM holds TWO accumulators
+//     (2 x 2 halves x BN <= 512 columns): the MMA warp starts tile i+1 while the
+//     epilogue warps drain tile i.
+namespace v2 {
+
+constexpr int RA = 6;   // raw-A ring (cp.async, also the TF32 "hi" operand)
+constexpr int RL = 2;   // A "lo" ring (computed by the producers)
+constexpr int RW = 3;   // W panel ring (TMA bulk copies)
+constexpr int kWarpW = 9;                  // W-panel loader warp
+constexpr int kEpi2 = 10;                  // 8 epilogue warps 10..17: (lane quarter, M half)
+constexpr int kEpiWarps2 = 8;
+constexpr int kThreads2 = 18 * 32;
+constexpr int kProducerThreads = kProducerWarps * 32;
+
+template <int BN>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 4;  // one raw / lo slot (256 x 16 fp32)
+  static constexpr int W_BYTES = BN * BK * 4;  // one of W hi / lo
+  static constexpr int RAW_OFF = 0;
+  static constexpr int LO_OFF = RA * A_BYTES;
+  static constexpr int W_OFF = LO_OFF + RL * A_BYTES;
+  static constexpr int EPI_OFF = W_OFF + RW * 2 * W_BYTES;
+  static constexpr uint32_t ACC = 2 * BN;      // TMEM columns of one accumulator
+  static constexpr uint32_t TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128
+                                    : 2 * ACC <= 256 ? 256 : 512;
+  static constexpr int EPI_BYTES = kEpiWarps2 * 32 * EPI_LD * 4 + kEpiWarps2 * BN * 4;
+  static constexpr int SMEM = EPI_OFF + EPI_BYTES;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>(HALF >> 4) << 24);
+};
+
+__global__ void w_panel_kernel(int N, int K, const float* __restrict__ W, int64_t ldw, int bn,
+                               int nkb, uint8_t* __restrict__ panel) {
+  const int blk = blockIdx.x;
+  const int nt = blk / nkb;
+  const int kb = blk - nt * nkb;
+  uint8_t* hi = panel + static_cast<int64_t>(blk) * 2 * bn * BK * 4;
+  uint8_t* lo = hi + bn * BK * 4;
+  for (int item = threadIdx.x; item < bn * 4; item += blockDim.x) {
+    const int r = item >> 2, c = item & 3;
+    const int n = nt * bn + r;
+    const int k = kb * BK + 4 * c;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n < N) v = load4<false>(W + static_cast<int64_t>(n) * ldw, k, K);
+    split_store(hi, lo, tile_off(r, c), v);
+  }
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Epilogue of one CW-column chunk (CW = 32 or 16) of a 32-row TMEM lane quarter.
+template <int CW, int ACT>
+__device__ __forceinline__ void epi_chunk(const TcArgs& a, uint32_t taddr, float* stage,
+                                          const float* bias_s, bool has_bias, int64_t row_base,
+                                          int col0, int lane) {
+  float v[CW];
+  if constexpr (CW == 32) tmem_ld32(taddr, v);
+  else tmem_ld16(taddr, v);
+#pragma unroll
+  for (int i = 0; i < CW; ++i) {
+    const int col = col0 + i;
+    v[i] = col < a.N ? epilogue_op<ACT>(v[i], bias_s + i, has_bias) : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < CW / 4; ++i)
+    *reinterpret_cast<float4*>(stage + lane * EPI_LD + 4 * i) =
+        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  __syncwarp();
+  constexpr int LPRW = CW / 4;          // lanes per row segment
+  constexpr int RPI = 32 / LPRW;        // rows per store instruction
+  const int cc = (lane % LPRW) * 4;
+  const int col = col0 + cc;
+#pragma unroll
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int rr = lane / LPRW + RPI * i;
+    const int64_t row = row_base + rr;
+    if (row < a.M && col < a.N) {
+      const float4 t = *reinterpret_cast<const float4*>(stage + rr * EPI_LD + cc);
+      float* dst = a.C + row * a.ldc + col;
+      if (a.c_vec4 && col + 3 < a.N) {
+        *reinterpret_cast<float4*>(dst) = t;
+      } else {
+        dst[0] = t.x;
+        if (col + 1 < a.N) dst[1] = t.y;
+        if (col + 2 < a.N) dst[2] = t.z;
+        if (col + 3 < a.N) dst[3] = t.w;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int BN, int ACT>
+__global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const uint8_t* __restrict__ panel) {
+  using C = Cfg2<BN>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t raw_empty[RA];
+  __shared__ __align__(8) uint64_t lo_full[RL], lo_empty[RL];
+  __shared__ __align__(8) uint64_t w_full[RW], w_empty[RW];
+  __shared__ __align__(8) uint64_t tmem_full[2];
+  __shared__ __align__(8) uint64_t tmem_empty[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :
+                 : "r"(smem_addr(&tmem_slot)), "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RA; ++i) mbar_init(&raw_empty[i], 1);           // tcgen05.commit
+    for (int i = 0; i < RL; ++i) {
+      mbar_init(&lo_full[i], kProducerWarps);                           // one per producer warp
+      mbar_init(&lo_empty[i], 1);
+    }
+    for (int i = 0; i < RW; ++i) {
+      mbar_init(&w_full[i], 1);                                         // expect_tx arrive
+      mbar_init(&w_empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], kEpiWarps2);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int nkb = a.nkb;
+  const int64_t my_tiles = blockIdx.x < a.num_tiles
+                               ? (a.num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * nkb;
+
+  if (a.mma_only && (warp < kProducerWarps || warp == kWarpW)) {
+    // diagnostics: no operand traffic
+  } else if (warp < kProducerWarps) {
+    // ---------------------------------------------------------- producers
+    // Thread t owns 16-byte chunks q = t + 256 i (i < 4) of every k-step:
+    // row q >> 2, k-chunk q & 3 -- it copies them (cp.async) and later turns
+    // the same chunks into lo, so it only ever waits on its own copies.
+    const int t = threadIdx.x;
+    int rows[4], chs[4];
+    uint32_t offs[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q = t + kProducerThreads * i;
+      rows[i] = q >> 2;
+      chs[i] = q & 3;
+      offs[i] = (rows[i] >= HALF ? C::A_BYTES / 2 : 0) + tile_off(rows[i] & (HALF - 1), chs[i]);
+    }
+    const uint32_t raw_base = smem_addr(smem + C::RAW_OFF);
+    auto issue = [&](int64_t idx) {
+      const int slot = static_cast<int>(idx % RA);
+      const uint32_t use = static_cast<uint32_t>(idx / RA);
+      mbar_wait(&raw_empty[slot], (use & 1u) ^ 1u);
+      const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
+      const int kb = static_cast<int>(idx % nkb);
+      const int64_t m0 = (tile / a.n_tiles) * BM;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t row = m0 + rows[i];
+        const int k = kb * BK + 4 * chs[i];
+        const bool ok = row < a.M && k < a.K;
+        const float* src = ok ? a.A + (a.a_rows ? a.a_rows[row] : row) * a.lda + k : a.A;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                     ::"r"(raw_base + slot * C::A_BYTES + offs[i]), "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    };
+    for (int64_t d = 0; d < RA - 1; ++d) {
+      if (d < total) issue(d);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int64_t idx = 0; idx < total; ++idx) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(RA - 2) : "memory");  // own copies of idx landed
+      const int rs = static_cast<int>(idx % RA);
+      const int ls = static_cast<int>(idx % RL);
+      const uint32_t luse = static_cast<uint32_t>(idx / RL);
+      mbar_wait(&lo_empty[ls], (luse & 1u) ^ 1u);
+      const uint8_t* raw = smem + C::RAW_OFF + rs * C::A_BYTES;
+      uint8_t* lo = smem + C::LO_OFF + ls * C::A_BYTES;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(raw + offs[i]);
+        float4 l;
+        l.x = __fsub_rn(v.x, __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+        l.y = __fsub_rn(v.y, __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+        l.z = __fsub_rn(v.z, __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+        l.w = __fsub_rn(v.w, __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+        *reinterpret_cast<float4*>(lo + offs[i]) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lo_full[ls]);
+      if (idx + RA - 1 < total) issue(idx + RA - 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else if (warp == kWarpW) {
+    // ------------------------------------------------- W panel loader (TMA)
+    if (lane == 0) {
+      for (int64_t idx = 0; idx < total; ++idx) {
+        const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
+        const int nt = static_cast<int>(tile % a.n_tiles);
+        const int kb = static_cast<int>(idx % nkb);
+        const int s = static_cast<int>(idx % RW);
+        const uint32_t use = static_cast<uint32_t>(idx / RW);
+        mbar_wait(&w_empty[s], (use & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&w_full[s], 2 * C::W_BYTES);
+        bulk_g2s(smem + C::W_OFF + s * 2 * C::W_BYTES,
+                 panel + (static_cast<int64_t>(nt) * nkb + kb) * 2 * C::W_BYTES, 2 * C::W_BYTES,
+                 &w_full[s]);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issue
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      const int buf = static_cast<int>(it & 1);
+      const uint32_t tuse = static_cast<uint32_t>(it >> 1);
+      mbar_wait(&tmem_empty[buf], (tuse & 1u) ^ 1u);
+      fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int64_t idx = it * nkb + kb;
+        const int rs = static_cast<int>(idx % RA);
+        const int ls = static_cast<int>(idx % RL);
+        const int ws = static_cast<int>(idx % RW);
+        if (!a.mma_only) {   // a.mma_only: diagnostics, MMA issue rate without operand waits
+          mbar_wait(&lo_full[ls], static_cast<uint32_t>(idx / RL) & 1u);
+          mbar_wait(&w_full[ws], static_cast<uint32_t>(idx / RW) & 1u);
+        }
+        fence_after();
+        if (lane == 0) {
+          const uint32_t a_hi = smem_addr(smem + C::RAW_OFF + rs * C::A_BYTES);
+          const uint32_t a_lo = smem_addr(smem + C::LO_OFF + ls * C::A_BYTES);
+          const uint32_t w_hi = smem_addr(smem + C::W_OFF + ws * 2 * C::W_BYTES);
+          const uint32_t w_lo = w_hi + C::W_BYTES;
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t step = j * 256;
+            const uint64_t dwh = umma_desc(w_hi + step);
+            const uint64_t dwl = umma_desc(w_lo + step);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t hoff = h * (C::A_BYTES / 2) + step;
+              const uint32_t d = tmem + static_cast<uint32_t>(buf * C::ACC + h * BN);
+              mma_tf32(d, umma_desc(a_lo + hoff), dwh, C::IDESC, (kb | j) != 0);
+              mma_tf32(d, umma_desc(a_hi + hoff), dwl, C::IDESC, 1u);
+              mma_tf32(d, umma_desc(a_hi + hoff), dwh, C::IDESC, 1u);
+            }
+          }
+          mma_commit(&raw_empty[rs]);
+          mma_commit(&lo_empty[ls]);
+          mma_commit(&w_empty[ws]);
+          if (kb == nkb - 1) mma_commit(&tmem_full[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    // 8 warps: warp w drains TMEM lane quarter (w % 4) (the tcgen05.ld access
+    // rule) of M half h = (w - kEpi2) / 4, i.e. 32 rows x BN columns.
+    const int q = warp & 3;
+    const int h = (warp - kEpi2) >> 2;
+    float* stage = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - kEpi2) * 32 * EPI_LD;
+    float* bias_s = reinterpret_cast<float*>(smem + C::EPI_OFF) + kEpiWarps2 * 32 * EPI_LD +
+                    (warp - kEpi2) * BN;
+    const bool has_bias = a.bias != nullptr;
+    int bias_n0 = -1;
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      const int buf = static_cast<int>(it & 1);
+      const uint32_t tuse = static_cast<uint32_t>(it >> 1);
+      const int64_t m0 = (tile / a.n_tiles) * BM;
+      const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
+      if (has_bias && n0 != bias_n0) {
+        __syncwarp();
+        for (int i = lane; i < BN; i += 32) bias_s[i] = n0 + i < a.N ? __ldg(a.bias + n0 + i) : 0.f;
+        __syncwarp();
+        bias_n0 = n0;
+      }
+      mbar_wait(&tmem_full[buf], tuse & 1u);
+      fence_after();
+      {
+        const int64_t row_base = m0 + h * HALF + q * 32;
+        const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                               static_cast<uint32_t>(buf * C::ACC + h * BN);
+#pragma unroll 1
+        for (int c0 = 0; c0 + 32 <= BN; c0 += 32)
+          epi_chunk<32, ACT>(a, tbase + c0, stage, bias_s + c0, has_bias, row_base, n0 + c0, lane);
+        if constexpr (BN % 32 == 16)
+          epi_chunk<16, ACT>(a, tbase + (BN - 16), stage, bias_s + (BN - 16), has_bias, row_base,
+                             n0 + BN - 16, lane);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" : : "r"(tmem), "r"(C::TCOLS));
+  }
+}
+
+template <int BN, int ACT>
+int launch_v2(TcArgs a, cudaStream_t s) {
+  using C = Cfg2<BN>;
+  static bool configured = false;
+  if (!configured) {
+    GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
+  a.num_tiles = ceil_div(a.M, BM) * a.n_tiles;
+  a.nkb = static_cast<int>(ceil_div(a.K, BK));
+  const size_t panel_bytes = static_cast<size_t>(a.n_tiles) * a.nkb * 2 * C::W_BYTES;
+  void* panel = nullptr;
+  GLINT_CUDA(cudaMallocAsync(&panel, panel_bytes, s));
+  w_panel_kernel<<<a.n_tiles * a.nkb, 128, 0, s>>>(a.N, a.K, a.W, a.ldw, BN, a.nkb,
+                                                   static_cast<uint8_t*>(panel));
+  int rc = launch_status("linear_3xtf32_panel");
+  if (rc == GLINT_OK) {
+    const int64_t grid = std::min<int64_t>(a.num_tiles, sm_count());
+    gemm_v2_kernel<BN, ACT><<<static_cast<unsigned>(grid), kThreads2, C::SMEM, s>>>(
+        a, static_cast<const uint8_t*>(panel));
+    rc = launch_status("linear_3xtf32");
+  }
+  GLINT_CUDA(cudaFreeAsync(panel, s));
+  return rc;
+}
+
+template <int BN>
+int launch_v2_act(const TcArgs& a, int act, cudaStream_t s) {
+  if (act == GLINT_ACT_RELU) return launch_v2<BN, GLINT_ACT_RELU>(a, s);
+  if (act == GLINT_ACT_LEAKY_RELU) return launch_v2<BN, GLINT_ACT_LEAKY_RELU>(a, s);
+  return launch_v2<BN, GLINT_ACT_NONE>(a, s);
+}
+
+// BN = N split into ceil(N/128) tiles, rounded up to an instantiated width.
+int launch_v2_bn(const TcArgs& a, int act, cudaStream_t s) {
+  const int nt = static_cast<int>(ceil_div(a.N, 128));
+  const int per = static_cast<int>(ceil_div(a.N, nt));
+  if (per <= 32) return launch_v2_act<32>(a, act, s);
+  if (per <= 48) return launch_v2_act<48>(a, act, s);
+  if (per <= 64) return launch_v2_act<64>(a, act, s);
+  if (per <= 96) return launch_v2_act<96>(a, act, s);
+  return launch_v2_act<128>(a, act, s);
+}
+
+}  // namespace v2
+
 }  // namespace
 
 int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
@@ -500,13 +903,17 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
   a.C = C;
   a.ldc = ldc;
   a.c_vec4 = (ldc % 4 == 0) && aligned16(C);
+  a.raw_hi = tuning(GLINT_TUNE_GEMM_RAWHI) != 0;
+  a.mma_only = tuning(GLINT_TUNE_GEMM_PROF) == 2;
   a.prof = nullptr;
-  if (tuning(GLINT_TUNE_GEMM_PROF)) {
+  if (tuning(GLINT_TUNE_GEMM_PROF) == 1) {
     void* p = nullptr;
     GLINT_CUDA(cudaGetSymbolAddress(&p, g_gemm_prof));
     a.prof = static_cast<unsigned long long*>(p);
   }
   const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
+  // v2 (double-buffered TMEM, TMA-fed W panel) unless the knob asks for v1
+  if (vec && tuning(GLINT_TUNE_GEMM_V1) == 0) return v2::launch_v2_bn(a, act, s);
   return vec ? launch_bn<true>(a, act, s) : launch_bn<false>(a, act, s);
 }
 

@@ -44,7 +44,7 @@ def main():
     ap.add_argument("--what", default="spmm,gemm")
     ap.add_argument("--dims", default="100,256,48")
     ap.add_argument("--variants", type=int, default=5)
-    ap.add_argument("--gemm", default="100x256,256x256,256x47")
+    ap.add_argument("--gemm", default="100x256,256x256,256x47,256x192,100x192")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
     n = args.nodes
@@ -193,7 +193,7 @@ def sweep_gat(args, g, n):
 def gemm_only(args, n):
     import torch
 
-    from paper_2211_15082_b200 import kernels
+    from paper_2211_15082_b200 import _lib, kernels
 
     for x in args.gemm.split(","):
         K, N = (int(v) for v in x.split("x"))
@@ -201,9 +201,23 @@ def gemm_only(args, n):
         w = torch.randn((N, K), device="cuda") / K ** 0.5
         b = torch.randn((N,), device="cuda")
         c = torch.empty((n, (N + 3) // 4 * 4), device="cuda")[:, :N]
+        outs = []
+        for v1 in (0, 1):
+            _lib.call("glint_set_tuning", 4, v1)
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
+            outs.append(c.clone())
+            print(json.dumps({"kernel": "linear", "K": K, "N": N, "precision": 1,
+                              "impl": "v1" if v1 else "v2", "ms": ms,
+                              "TFLOPs": 2 * n * K * N / ms / 1e9,
+                              "GBps": (n * K * 4 + n * N * 4) / ms / 1e6}), flush=True)
+        _lib.call("glint_set_tuning", 4, 0)
+        _lib.call("glint_set_tuning", 1, 2)     # v2 with MMA issue only (no operand traffic)
         ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
-        print(json.dumps({"kernel": "linear", "K": K, "N": N, "precision": 1, "ms": ms,
+        _lib.call("glint_set_tuning", 1, 0)
+        print(json.dumps({"kernel": "linear_mma_only", "K": K, "N": N, "ms": ms,
                           "TFLOPs": 2 * n * K * N / ms / 1e9}), flush=True)
+        print(json.dumps({"kernel": "linear_v1_v2_identical", "K": K, "N": N,
+                          "identical": bool(torch.equal(outs[0], outs[1]))}), flush=True)
 
 
 if __name__ == "__main__":
