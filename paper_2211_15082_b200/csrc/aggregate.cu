@@ -813,6 +813,8 @@ struct GatArgs {
   float* __restrict__ out;
   int64_t ld_out;
   int act;
+  bool diag_nopeak;  // diagnostics (GLINT_TUNE_GAT_DIAG 1): async kernel skips pass 1 (wrong results)
+  bool diag_noexp;   // diagnostics (GLINT_TUNE_GAT_DIAG 2): ... and uses the raw score as weight
 };
 
 __device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
@@ -1013,6 +1015,163 @@ __device__ __forceinline__ void gat_row_hub(const GatArgs& a, int64_t r, int col
     const float n = __fadd_rn(num, __fmul_rn(ws, __ldg(a.Z + self * a.ldz + zc)));
     a.out[r * a.ld_out + hh * a.head_dim + j] = gat_epilogue(a, __fdiv_rn(n, d));
   }
+}
+
+// Regular GAT row through a per-lane cp.async ring (as mean_row_async): lane
+// g owns the 16-byte Z chunks g, g+LPR, ...; per edge it copies its chunks AND
+// the source score s_src[u, head(chunk)] (4 bytes) into ring slot (edge % R),
+// R-1 edges ahead, and at consume time turns the score into the softmax
+// weight itself -- the same expression as gat_row_regular's, so the bytes
+// match it; accumulation in stored edge order, self last.
+template <int H, int LPR, int VPL, int R>
+__device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int lane_g,
+                                              unsigned gmask, float4* zring, float* sgrp) {
+  // sgrp: this group's score slots, slot t at sgrp[t * 32 + h]
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  const int deg = static_cast<int>(end - beg);
+
+  // pass 1: per-head peak over self + edges (order-free), two index loads in flight
+  float sd_k[VPL], pk_k[VPL];
+  int hk[VPL];
+  bool ok[VPL];
+  {
+    float sdst[H], peak[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      sdst[h] = __ldg(a.s_dst + self * H + h);
+      peak[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope);
+    }
+    for (int e = lane_g; e < (a.diag_nopeak ? 0 : deg); e += 2 * LPR) {
+      const int64_t u0 = a.ra.map(a.ra.indices[beg + e]);
+      const bool two = e + LPR < deg;
+      const int64_t u1 = two ? a.ra.map(a.ra.indices[beg + e + LPR]) : u0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const float s0 = __ldg(a.s_src + u0 * H + h);
+        const float s1 = __ldg(a.s_src + u1 * H + h);
+        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s0, sdst[h]), a.slope));
+        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s1, sdst[h]), a.slope));
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1)
+        peak[h] = fmaxf(peak[h], __shfl_xor_sync(gmask, peak[h], o, LPR));
+    }
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int zc = (lane_g + LPR * k) * 4;
+      ok[k] = zc < H * a.head_pitch;
+      hk[k] = ok[k] ? zc / a.head_pitch : 0;
+      sd_k[k] = sdst[0];
+      pk_k[k] = peak[0];
+#pragma unroll
+      for (int h = 1; h < H; ++h)
+        if (h == hk[k]) { sd_k[k] = sdst[h]; pk_k[k] = peak[h]; }
+    }
+  }
+
+  const uint32_t zr = smem_u32(zring), sr = smem_u32(sgrp);
+  int ie = 0, cb = 0;
+  int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
+  int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
+  auto issue = [&](int slot) {
+    if (ie - cb == LPR) {
+      cb += LPR;
+      cur = nxt;
+      nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
+    }
+    const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
+    const float* zsrc = a.Z + u * a.ldz + lane_g * 4;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (ok[k]) {
+        const uint32_t o = static_cast<uint32_t>((slot * VPL + k) * kThreads);
+        cp_async16(zr + o * 16u, zsrc + LPR * 4 * k);
+      }
+    }
+    if (lane_g < H)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
+                   ::"r"(sr + static_cast<uint32_t>(slot * 32 + lane_g) * 4u), "l"(a.s_src + u * H + lane_g)
+                   : "memory");
+    ++ie;
+  };
+
+  float num[VPL][4], den[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    den[k] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) num[k][c] = 0.0f;
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    if (ie < deg) issue(t);
+    cp_async_commit();
+  }
+  int slot = 0;
+  for (int j = 0; j < deg; ++j) {
+    cp_async_wait<R - 1>();
+    __syncwarp(gmask);   // the group's score copies for this edge have landed
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (ok[k]) {
+        const int o = (slot * VPL + k) * kThreads;
+        const float4 v = zring[o];
+        const float sv = sgrp[slot * 32 + hk[k]];
+        const float w = a.diag_noexp ? sv
+                                     : expf(__fsub_rn(leaky(__fadd_rn(sv, sd_k[k]), a.slope), pk_k[k]));
+        den[k] = __fadd_rn(den[k], w);
+        num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v.x));
+        num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v.y));
+        num[k][2] = __fadd_rn(num[k][2], __fmul_rn(w, v.z));
+        num[k][3] = __fadd_rn(num[k][3], __fmul_rn(w, v.w));
+      }
+    }
+    __syncwarp(gmask);   // every lane is done with the slot before it is refilled
+    if (ie < deg) issue(slot);
+    cp_async_commit();
+    slot = (slot + 1 == R) ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    if (!ok[k]) continue;
+    const int zc = (lane_g + LPR * k) * 4;
+    const int hh = hk[k];
+    const int jc = zc - hh * a.head_pitch;
+    const float4 zs = ldg_f4(a.Z + self * a.ldz + zc);
+    const float ws = expf(__fsub_rn(
+        leaky(__fadd_rn(__ldg(a.s_src + self * H + hh), sd_k[k]), a.slope), pk_k[k]));
+    const float d = __fadd_rn(den[k], ws);
+    const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
+    float* dst = a.out + r * a.ld_out + hh * a.head_dim + jc;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (jc + c < a.head_dim)
+        dst[c] = gat_epilogue(a, __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d));
+  }
+}
+
+template <int H, int LPR, int VPL, int R, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) gat_async_kernel(GatArgs a) {
+  extern __shared__ __align__(16) float4 gring[];
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
+  const int64_t idx = a.sc.n_hub + slot;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  float* sbase = reinterpret_cast<float*>(gring + R * VPL * kThreads) + warp * R * 32 + group * LPR;
+  gat_row_async<H, LPR, VPL, R>(a, r, lane_g, gmask, gring + threadIdx.x, sbase);
 }
 
 // Hub rows (first n_hub schedule entries): one CTA per (row, 256-column block).
@@ -1217,7 +1376,10 @@ __global__ void __launch_bounds__(kThreads, MINB) gat_kernel(GatArgs a) {
   gat_row_regular<H, LPR, VPL, U>(a, r, lane_g, gmask, w_s, s_st[warp * G + group]);
 }
 
-template <int H, int LPR, int VPL, int U, int MINB>
+// Regular rows on the caller's stream (R == 0: register-staged kernel with U
+// loads in flight; R > 0: per-lane cp.async ring of R edges), hub rows on the
+// library side stream, concurrently.
+template <int H, int LPR, int VPL, int U, int MINB, int R = 0>
 int launch_gat(const GatArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
   const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
@@ -1237,7 +1399,19 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
     if (rc) return rc;
     GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   }
-  if (grid > 0) gat_kernel<H, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  if constexpr (R == 0) {
+    if (grid > 0) gat_kernel<H, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  } else {
+    constexpr int smem = R * VPL * kThreads * 16 + R * kThreads * 4;  // Z chunks + group scores
+    static bool configured = false;
+    if (!configured) {
+      GLINT_CUDA(cudaFuncSetAttribute(gat_async_kernel<H, LPR, VPL, R, MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured = true;
+    }
+    if (grid > 0)
+      gat_async_kernel<H, LPR, VPL, R, MINB><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  }
   const int rc = launch_status("gat_aggregate");
   if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
   return rc;
@@ -1253,12 +1427,18 @@ int dispatch_gat_h(const GatArgs& a, int chunks, cudaStream_t s) {
   if (chunks <= 32) {
     if (v == 1) return launch_gat<H, 32, 1, 8, 4>(a, s);
     if (v == 2) return launch_gat<H, 16, 2, 4, 5>(a, s);
+    if (v == 5) return launch_gat<H, 32, 1, 0, 4, 8>(a, s);
     return launch_gat<H, 32, 1, 4, 6>(a, s);
   }
   if (chunks <= 48) {
     if (v == 1) return launch_gat<H, 16, 3, 3, 3>(a, s);
     if (v == 2) return launch_gat<H, 32, 2, 3, 4>(a, s);
     if (v == 3) return launch_gat<H, 16, 3, 2, 5>(a, s);
+    if (v == 4) return launch_gat<H, 16, 3, 2, 4>(a, s);
+    if (v == 5) return launch_gat<H, 16, 3, 0, 3, 6>(a, s);
+    if (v == 6) return launch_gat<H, 16, 3, 0, 4, 4>(a, s);
+    if (v == 7) return launch_gat<H, 32, 2, 0, 4, 6>(a, s);
+    if (v == 8) return launch_gat<H, 32, 2, 0, 3, 8>(a, s);
     return launch_gat<H, 16, 3, 2, 4>(a, s);
   }
   if (chunks <= 64) {
@@ -1266,6 +1446,10 @@ int dispatch_gat_h(const GatArgs& a, int chunks, cudaStream_t s) {
     if (v == 2) return launch_gat<H, 32, 2, 2, 5>(a, s);
     if (v == 3) return launch_gat<H, 32, 2, 4, 4>(a, s);
     if (v == 4) return launch_gat<H, 32, 2, 3, 5>(a, s);
+    if (v == 5) return launch_gat<H, 32, 2, 0, 4, 4>(a, s);
+    if (v == 6) return launch_gat<H, 32, 2, 0, 3, 6>(a, s);
+    if (v == 7) return launch_gat<H, 32, 2, 0, 4, 6>(a, s);
+    if (v == 8) return launch_gat<H, 32, 2, 0, 3, 8>(a, s);
     return launch_gat<H, 32, 2, 3, 4>(a, s);
   }
   if (chunks <= 128) return launch_gat<H, 32, 4, 2, 3>(a, s);
@@ -1382,6 +1566,8 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
   a.ld_out = ld_out;
   GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "gat_aggregate: bad act %d", act);
   a.act = act;
+  a.diag_nopeak = tuning(GLINT_TUNE_GAT_DIAG) >= 1;
+  a.diag_noexp = tuning(GLINT_TUNE_GAT_DIAG) == 2;
   const int zw = heads * head_pitch;
   a.sc.schedule = schedule;
   a.sc.n_rows = n_rows;

@@ -255,10 +255,19 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(torch.relu(outs[0]), outs[2])
     assert torch.equal(outs[0], outs[3])
-    # and the same bytes without any hub path (every row in the regular kernel)
-    plain = torch.empty_like(outs[0])
-    kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n)
-    assert torch.equal(plain, outs[0])
+    # and the same bytes without any hub path (every row in the regular kernel),
+    # for every launch variant (register-staged and cp.async ring)
+    try:
+        for v in range(9):
+            _lib.call("glint_set_tuning", 3, v)
+            plain = torch.empty_like(outs[0])
+            kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n)
+            assert torch.equal(plain, outs[0]), v
+            kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n,
+                                  schedule=sched, n_hub=int(nh.item()))
+            assert torch.equal(plain, outs[0]), v
+    finally:
+        _lib.call("glint_set_tuning", 3, 0)
 
 
 def test_attn_zero_logits_equal_mean_after_transform(cuda):
