@@ -813,8 +813,6 @@ struct GatArgs {
   float* __restrict__ out;
   int64_t ld_out;
   int act;
-  bool diag_nopeak;  // diagnostics (GLINT_TUNE_GAT_DIAG 1): async kernel skips pass 1 (wrong results)
-  bool diag_noexp;   // diagnostics (GLINT_TUNE_GAT_DIAG 2): ... and uses the raw score as weight
 };
 
 __device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
@@ -1044,7 +1042,7 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       sdst[h] = __ldg(a.s_dst + self * H + h);
       peak[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope);
     }
-    for (int e = lane_g; e < (a.diag_nopeak ? 0 : deg); e += 2 * LPR) {
+    for (int e = lane_g; e < deg; e += 2 * LPR) {
       const int64_t u0 = a.ra.map(a.ra.indices[beg + e]);
       const bool two = e + LPR < deg;
       const int64_t u1 = two ? a.ra.map(a.ra.indices[beg + e + LPR]) : u0;
@@ -1122,9 +1120,8 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       if (ok[k]) {
         const int o = (slot * VPL + k) * kThreads;
         const float4 v = zring[o];
-        const float sv = sgrp[slot * 32 + hk[k]];
-        const float w = a.diag_noexp ? sv
-                                     : expf(__fsub_rn(leaky(__fadd_rn(sv, sd_k[k]), a.slope), pk_k[k]));
+        const float w = expf(__fsub_rn(leaky(__fadd_rn(sgrp[slot * 32 + hk[k]], sd_k[k]), a.slope),
+                                       pk_k[k]));
         den[k] = __fadd_rn(den[k], w);
         num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v.x));
         num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v.y));
@@ -1566,8 +1563,6 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
   a.ld_out = ld_out;
   GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "gat_aggregate: bad act %d", act);
   a.act = act;
-  a.diag_nopeak = tuning(GLINT_TUNE_GAT_DIAG) >= 1;
-  a.diag_noexp = tuning(GLINT_TUNE_GAT_DIAG) == 2;
   const int zw = heads * head_pitch;
   a.sc.schedule = schedule;
   a.sc.n_rows = n_rows;

@@ -186,15 +186,6 @@ def sweep_gat(args, g, n):
             print(json.dumps({"kernel": "gat_aggregate", "heads": heads, "head_dim": dh,
                               "variant": variant, "ms": ms, "GBps": nb / ms / 1e6,
                               "identical_to_v0": same}), flush=True)
-        for variant, diag in ((5, 1), (6, 1), (5, 2), (6, 2)):  # ring kernel diagnostics
-            _lib.call("glint_set_tuning", 3, variant)
-            _lib.call("glint_set_tuning", 6, diag)
-            ms = timed(run, args.reps)
-            _lib.call("glint_set_tuning", 6, 0)
-            print(json.dumps({"kernel": "gat_aggregate_diag" + ("_nopeak" if diag == 1 else "_noexp"),
-                              "heads": heads, "head_dim": dh, "variant": variant, "ms": ms,
-                              "GBps": agg_bytes(heads * hp, g.num_edges, n, heads=heads) / ms / 1e6}),
-                  flush=True)
         _lib.call("glint_set_tuning", 3, 0)
         del Z, out, ref
 
