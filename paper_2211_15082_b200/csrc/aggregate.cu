@@ -490,9 +490,11 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int LPR, int VPL, int R>
+template <int LPR, int VPL, int R, int STRIDE = kThreads, int B = 1>
 __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int lane_g,
-                                               unsigned gmask, float4* ring) {
+                                               unsigned gmask, float4* ring, int col0 = 0) {
+  // ring: this lane's slots, slot (t, k) at ring[(t * VPL + k) * STRIDE]; the
+  // lane's column chunks start at col0 (hub units cover one column block)
   const int64_t rid = a.ra.csr_row(r);
   const int64_t beg = a.ra.indptr[rid];
   const int64_t end = a.ra.indptr[rid + 1];
@@ -500,8 +502,8 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   const int deg = static_cast<int>(end - beg);
   bool ok[VPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) ok[k] = (lane_g + LPR * k) * 4 < a.dim;
-  const uint32_t ring_s = smem_u32(ring);  // slot (t, k) at ring + (t*VPL + k) * kThreads
+  for (int k = 0; k < VPL; ++k) ok[k] = col0 + (lane_g + LPR * k) * 4 < a.dim;
+  const uint32_t ring_s = smem_u32(ring);
 
   // issue cursor: edge `ie`, index chunk [cb, cb+LPR) held in `cur`, next in `nxt`
   int ie = 0, cb = 0;
@@ -514,11 +516,11 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
     }
     const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
-    const float* src = a.h + u * a.ld_h + lane_g * 4;
+    const float* src = a.h + u * a.ld_h + col0 + lane_g * 4;
 #pragma unroll
     for (int k = 0; k < VPL; ++k)
       if (ok[k])
-        cp_async16(ring_s + static_cast<uint32_t>((slot * VPL + k) * kThreads) * 16u,
+        cp_async16(ring_s + static_cast<uint32_t>((slot * VPL + k) * STRIDE) * 16u,
                    src + LPR * 4 * k);
     ++ie;
   };
@@ -529,33 +531,51 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[k][c] = 0.0f;
 
+  // Edges move in batches of B (one cp.async group each, R/B groups in
+  // flight): one wait per batch, B independent shared loads ahead of the
+  // in-order adds, so a lone warp (hub rows) is not bound by per-edge latency.
+  constexpr int NG = R / B;
+  static_assert(NG * B == R, "ring depth must be a multiple of the batch");
 #pragma unroll
-  for (int t = 0; t < R; ++t) {
-    if (ie < deg) issue(t);
+  for (int g = 0; g < NG; ++g) {
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (ie < deg) issue(g * B + b);
     cp_async_commit();
   }
-  int slot = 0;
-  for (int j = 0; j < deg; ++j) {
-    cp_async_wait<R - 1>();
+  int base = 0;
+  for (int j0 = 0; j0 < deg; j0 += B) {
+    cp_async_wait<NG - 1>();
+    float4 v[B][VPL];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      if (ok[k]) {
-        const float4 v = ring[(slot * VPL + k) * kThreads];
-        acc[k][0] = __fadd_rn(acc[k][0], v.x);
-        acc[k][1] = __fadd_rn(acc[k][1], v.y);
-        acc[k][2] = __fadd_rn(acc[k][2], v.z);
-        acc[k][3] = __fadd_rn(acc[k][3], v.w);
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        v[b][k] = (ok[k] && j0 + b < deg) ? ring[((base + b) * VPL + k) * STRIDE]
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (j0 + b < deg) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          acc[k][0] = __fadd_rn(acc[k][0], v[b][k].x);
+          acc[k][1] = __fadd_rn(acc[k][1], v[b][k].y);
+          acc[k][2] = __fadd_rn(acc[k][2], v[b][k].z);
+          acc[k][3] = __fadd_rn(acc[k][3], v[b][k].w);
+        }
       }
     }
-    if (ie < deg) issue(slot);
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (ie < deg) issue(base + b);
     cp_async_commit();
-    slot = (slot + 1 == R) ? 0 : slot + 1;
+    base = (base + B == R) ? 0 : base + B;
   }
   cp_async_wait<0>();
   const int64_t self_off = a.ra.self_row(r, rid) * a.ld_h;
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
-    const int col = (lane_g + LPR * k) * 4;
+    const int col = col0 + (lane_g + LPR * k) * 4;
     if (!ok[k]) continue;
     float sv[4];
     load_vec<4>(sv, a.h + self_off + col);
@@ -567,7 +587,7 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   }
 }
 
-template <int LPR, int VPL, int R, int MINB>
+template <int LPR, int VPL, int R, int MINB, int B = 1>
 __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) {
   extern __shared__ __align__(16) float4 ring_all[];
   constexpr int G = 32 / LPR;
@@ -580,16 +600,51 @@ __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) 
   if (idx >= a.sc.n_rows) return;
   const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
   const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
-  mean_row_async<LPR, VPL, R>(a, r, lane_g, gmask, ring_all + threadIdx.x);
+  mean_row_async<LPR, VPL, R, kThreads, B>(a, r, lane_g, gmask, ring_all + threadIdx.x);
 }
 
-template <int LPR, int VPL, int R, int MINB>
+// Hub rows, per-lane cp.async ring: one warp per (hub row, 128-column block),
+// each lane one 16-byte column chunk with kHubR row chunks in flight (a row's
+// bytes in flight = 4 d kHubR, so a 20K-neighbour row streams at ~deg/kHubR
+// latencies).  Persistent grid of 2 one-warp CTAs per SM walking the hub units
+// in the schedule's longest-first order: hub rows never occupy more than a
+// sliver of each SM, so the concurrent regular-row kernel keeps the rest.
+constexpr int kHubR = 64;
+
+__global__ void __launch_bounds__(32) mean_hub_async_kernel(MeanArgs a, int col_blocks,
+                                                            int64_t units) {
+  extern __shared__ __align__(16) float4 hring[];
+  for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int64_t hub = unit / col_blocks;
+    const int cb = static_cast<int>(unit - hub * col_blocks);
+    mean_row_async<32, 1, kHubR, 32, 8>(a, static_cast<int64_t>(a.sc.schedule[hub]), threadIdx.x,
+                                        0xffffffffu, hring + threadIdx.x, cb * 128);
+  }
+}
+
+int launch_hub_async(const MeanArgs& a, cudaStream_t s) {
+  constexpr int smem = kHubR * 32 * 16;
+  static bool configured = false;
+  if (!configured) {
+    GLINT_CUDA(cudaFuncSetAttribute(mean_hub_async_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const int col_blocks = static_cast<int>(ceil_div(a.dim, 128));
+  const int64_t units = a.sc.n_hub * col_blocks;
+  const int64_t grid = std::min<int64_t>(units, 2LL * sm_count());
+  if (grid <= 0) return GLINT_OK;
+  mean_hub_async_kernel<<<static_cast<unsigned>(grid), 32, smem, s>>>(a, col_blocks, units);
+  return launch_status("spmm_mean_hub_async");
+}
+
+template <int LPR, int VPL, int R, int MINB, int B = 1>
 int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
   constexpr int smem = R * VPL * kThreads * 16;
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB>,
+    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
@@ -599,7 +654,7 @@ int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
     set_error("spmm_mean: grid too large");
     return GLINT_EINVAL;
   }
-  mean_async_kernel<LPR, VPL, R, MINB><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  mean_async_kernel<LPR, VPL, R, MINB, B><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   return launch_status("spmm_mean_async");
 }
 
@@ -626,14 +681,20 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s);
 // rows' time and leaves shared memory to them (profiles/r01_spmm_sweep*.jsonl).
 int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
   if (a.sc.n_hub == 0) return dispatch_regular(a, vec4, s);
-  const int inline_knob = tuning(GLINT_TUNE_HUB_INLINE);  // 0 auto, 1 register, 2 bulk
-  const bool use_bulk = vec4 && (inline_knob >= 2 || (inline_knob == 0 && a.sc.n_rows < (1 << 19)));
+  // hub path: 0 auto = producer-warp ring CTAs on small launches (a hub row
+  // bounds them; ~35 ns per edge per CTA), register CTAs on large ones (best
+  // aggregate throughput, profiles/r01_spmm_sweep_async.jsonl); 1 register
+  // CTAs, 2/3/4 ring CTAs (LDGSTS 32-col / TMA 32-col / LDGSTS 64-col),
+  // 5 one-warp cp.async units (per-warp request limit: ~116 ns per edge).
+  const int knob = tuning(GLINT_TUNE_HUB_INLINE);
   SideStream* ss = nullptr;
   int rc = side_stream(&ss);
   if (rc) return rc;
   GLINT_CUDA(cudaEventRecord(ss->fork, s));
   GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-  if (use_bulk) {
+  if (vec4 && knob == 5) {
+    rc = launch_hub_async(a, ss->stream);
+  } else if (vec4 && (knob >= 2 || (knob == 0 && a.sc.n_rows < (1 << 19)))) {
     rc = launch_hub(a, ss->stream);
   } else {
     mean_hub_reg_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
@@ -668,7 +729,7 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
       if (variant == 10) return launch_mean_async<4, 4, 6, 2>(a, s);
       if (variant == 11) return launch_mean_async<16, 1, 12, 3>(a, s);
       if (variant == 9) return launch_mean_async<8, 2, 8, 3>(a, s);
-      if (variant == 13) return launch_mean_async<8, 2, 4, 6>(a, s);
+      if (variant == 13) return launch_mean_async<8, 2, 6, 4, 2>(a, s);
       if (variant == 14) return launch_mean_async<16, 1, 6, 5>(a, s);
       if (variant == 15) return launch_mean_async<4, 4, 4, 3>(a, s);
       return launch_mean_async<8, 2, 6, 4>(a, s);   // also variant 12
@@ -679,7 +740,7 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
       if (variant == 10) return launch_mean_async<8, 4, 6, 2>(a, s);
       if (variant == 11) return launch_mean_async<32, 1, 12, 3>(a, s);
       if (variant == 12) return launch_mean_async<32, 1, 6, 5>(a, s);
-      if (variant == 13) return launch_mean_async<32, 1, 4, 6>(a, s);
+      if (variant == 13) return launch_mean_async<32, 1, 8, 4, 2>(a, s);
       if (variant == 14) return launch_mean_async<16, 2, 6, 4>(a, s);
       if (variant == 15) return launch_mean_async<8, 4, 4, 3>(a, s);
       return launch_mean_async<32, 1, 8, 4>(a, s);   // also variant 8
@@ -690,7 +751,7 @@ int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
       if (variant == 10) return launch_mean_async<32, 2, 12, 2>(a, s);
       if (variant == 11) return launch_mean_async<32, 2, 10, 2>(a, s);
       if (variant == 12) return launch_mean_async<32, 2, 3, 5>(a, s);
-      if (variant == 13) return launch_mean_async<32, 2, 2, 8>(a, s);
+      if (variant == 13) return launch_mean_async<32, 2, 4, 4, 2>(a, s);
       if (variant == 14) return launch_mean_async<16, 4, 4, 3>(a, s);
       if (variant == 15) return launch_mean_async<32, 2, 5, 4>(a, s);
       return launch_mean_async<32, 2, 4, 4>(a, s);   // also variant 8

@@ -114,7 +114,7 @@ def test_agg_mean_every_variant_bit_exact(cuda, dim):
     sched, nh = kernels.degree_schedule(ip, None, 0, n)
     try:
         for variant in range(16):
-            for hub in (1, 2, 3, 4):
+            for hub in (0, 1, 2, 3, 4, 5):
                 _lib.call("glint_set_tuning", 0, variant)
                 _lib.call("glint_set_tuning", 2, hub)
                 out = torch.full((n, pitch), 7.0, dtype=torch.float32, device="cuda")
