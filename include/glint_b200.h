@@ -146,6 +146,18 @@ int glint_gat_scores_f32(int64_t M, int32_t heads, int32_t head_dim,
                          int32_t head_pitch, const float* Z, int64_t ldz,
                          const float* attn, float* s_src, float* s_dst,
                          glint_stream_t stream);
+/* Fused per-layer GAT projection (kernels.py:185-189 for all heads at once):
+ * Z = A W_pad^T with W_pad = [heads * head_pitch, K] (zero pad rows per head),
+ * and s_src / s_dst as glint_gat_scores_f32, computed in the GEMM epilogue
+ * while the Z tile is in registers (3xTF32 path; other precisions / shapes
+ * run glint_linear_f32 + glint_gat_scores_f32).  Scores are one sequential
+ * fmaf chain over j per (row, head). */
+int glint_gat_project_f32(int64_t M, int32_t heads, int32_t head_dim,
+                          int32_t head_pitch, int32_t K, const float* A,
+                          int64_t lda, const int64_t* a_rows, const float* W_pad,
+                          int64_t ldw, const float* attn, float* Z, int64_t ldz,
+                          float* s_src, float* s_dst, int32_t precision,
+                          glint_stream_t stream);
 /* Edge softmax + weighted sum over N(v) u {v} per head (kernels.py:190-202):
  * logit = LeakyReLU_slope(s_src[u,h] + s_dst[v,h]); peak = max(self, edges);
  * w = exp(logit - peak); out[r, h*head_dim + j] =

@@ -48,6 +48,8 @@ SIGNATURES = {
     "glint_linear_f32": (ctypes.c_int, [_I64, _I32, _I32, _P, _I64, _P, _P, _I64, _P, _I32,
                                         _P, _I64, _I32, _P]),
     "glint_gat_scores_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P]),
+    "glint_gat_project_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _I32, _P, _I64, _P, _P,
+                                             _I64, _P, _P, _I64, _P, _P, _I32, _P]),
     "glint_gat_aggregate_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _P, _P, _I64, _P,
                                                _P, _P, _I64, _P, _P, _F32, _P, _I64, _P, _I64,
                                                _I32, _P]),

@@ -148,6 +148,11 @@ struct TcArgs {
   bool c_vec4;
   bool raw_hi;               // experiment knob GLINT_TUNE_GEMM_RAWHI (v1 kernel only)
   bool mma_only;             // diagnostics knob GLINT_TUNE_GEMM_PROF == 2 (v2 kernel)
+  // GAT projection epilogue (v2, SC = true): per-head scores of each output row
+  const float* attn;         // [heads, 2 * head_dim]
+  float* s_src;              // [M, heads]
+  float* s_dst;
+  int heads, head_dim, head_pitch;
   unsigned long long* prof;  // optional phase-cycle counters (GLINT_TUNE_GEMM_PROF)
 };
 
@@ -514,6 +519,7 @@ constexpr int kEpi2 = 10;                  // 8 epilogue warps 10..17: (lane qua
 constexpr int kEpiWarps2 = 8;
 constexpr int kThreads2 = 18 * 32;
 constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kScMaxN = 512;               // widest Z row with the fused score epilogue
 
 template <int BN>
 struct Cfg2 {
@@ -527,7 +533,9 @@ struct Cfg2 {
   static constexpr uint32_t TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128
                                     : 2 * ACC <= 256 ? 256 : 512;
   static constexpr int EPI_BYTES = kEpiWarps2 * 32 * EPI_LD * 4 + kEpiWarps2 * BN * 4;
+  static constexpr int SC_OFF = EPI_OFF + EPI_BYTES;      // score tables (SC kernels only)
   static constexpr int SMEM = EPI_OFF + EPI_BYTES;
+  static constexpr int SMEM_SC = SC_OFF + 3 * kScMaxN * 4;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (static_cast<uint32_t>(BN >> 3) << 17) |
                                     (static_cast<uint32_t>(HALF >> 4) << 24);
@@ -565,10 +573,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 // Epilogue of one CW-column chunk (CW = 32 or 16) of a 32-row TMEM lane quarter.
-template <int CW, int ACT>
+// Running per-row GAT score state of the fused projection epilogue: the lane
+// walks its row's columns in order; a head's dot products with a_src / a_dst
+// are sequential fmaf chains over j, written out when the head ends.
+struct ScoreAcc {
+  int h;
+  float ps, pd;
+};
+
+__device__ __forceinline__ void score_flush(const TcArgs& a, ScoreAcc& st, int64_t row) {
+  if (st.h >= 0 && row < a.M) {
+    a.s_src[row * a.heads + st.h] = st.ps;
+    a.s_dst[row * a.heads + st.h] = st.pd;
+  }
+}
+
+template <int CW, int ACT, bool SC = false>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, uint32_t taddr, float* stage,
                                           const float* bias_s, bool has_bias, int64_t row_base,
-                                          int col0, int lane) {
+                                          int col0, int lane, const float* sc_tab,
+                                          ScoreAcc& st) {
   float v[CW];
   if constexpr (CW == 32) tmem_ld32(taddr, v);
   else tmem_ld16(taddr, v);
@@ -576,6 +600,25 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, uint32_t taddr, float
   for (int i = 0; i < CW; ++i) {
     const int col = col0 + i;
     v[i] = col < a.N ? epilogue_op<ACT>(v[i], bias_s + i, has_bias) : 0.0f;
+  }
+  if constexpr (SC) {
+    // sc_tab: [0, N) a_src per column, [kScMaxN, +N) a_dst, [2 kScMaxN, +N) head
+    const int64_t row = row_base + lane;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) {
+      const int col = col0 + i;
+      if (col < a.N) {
+        const int h = __float_as_int(sc_tab[2 * kScMaxN + col]);
+        if (h != st.h) {
+          score_flush(a, st, row);
+          st.h = h;
+          st.ps = 0.0f;
+          st.pd = 0.0f;
+        }
+        st.ps = fmaf(v[i], sc_tab[col], st.ps);
+        st.pd = fmaf(v[i], sc_tab[kScMaxN + col], st.pd);
+      }
+    }
   }
 #pragma unroll
   for (int i = 0; i < CW / 4; ++i)
@@ -618,7 +661,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <int BN, int ACT>
+template <int BN, int ACT, bool SC = false>
 __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const uint8_t* __restrict__ panel) {
   using C = Cfg2<BN>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -798,6 +841,19 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
     float* bias_s = reinterpret_cast<float*>(smem + C::EPI_OFF) + kEpiWarps2 * 32 * EPI_LD +
                     (warp - kEpi2) * BN;
     const bool has_bias = a.bias != nullptr;
+    float* sc_tab = reinterpret_cast<float*>(smem + C::SC_OFF);
+    if constexpr (SC) {
+      // per-column a_src / a_dst / head tables, shared by the 8 epilogue warps
+      for (int c = threadIdx.x - kEpi2 * 32; c < a.N; c += kEpiWarps2 * 32) {
+        const int hh = c / a.head_pitch;
+        const int j = c - hh * a.head_pitch;
+        const bool live = hh < a.heads && j < a.head_dim;
+        sc_tab[c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + j) : 0.0f;
+        sc_tab[kScMaxN + c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + a.head_dim + j) : 0.0f;
+        sc_tab[2 * kScMaxN + c] = __int_as_float(min(hh, a.heads - 1));
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(kEpiWarps2 * 32) : "memory");
+    }
     int bias_n0 = -1;
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
@@ -817,12 +873,15 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
         const int64_t row_base = m0 + h * HALF + q * 32;
         const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(buf * C::ACC + h * BN);
+        ScoreAcc st{-1, 0.0f, 0.0f};
 #pragma unroll 1
         for (int c0 = 0; c0 + 32 <= BN; c0 += 32)
-          epi_chunk<32, ACT>(a, tbase + c0, stage, bias_s + c0, has_bias, row_base, n0 + c0, lane);
+          epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_s + c0, has_bias, row_base, n0 + c0,
+                                 lane, sc_tab, st);
         if constexpr (BN % 32 == 16)
-          epi_chunk<16, ACT>(a, tbase + (BN - 16), stage, bias_s + (BN - 16), has_bias, row_base,
-                             n0 + BN - 16, lane);
+          epi_chunk<16, ACT, SC>(a, tbase + (BN - 16), stage, bias_s + (BN - 16), has_bias,
+                                 row_base, n0 + BN - 16, lane, sc_tab, st);
+        if constexpr (SC) score_flush(a, st, row_base + lane);
       }
       fence_before();
       __syncwarp();
@@ -837,13 +896,14 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   }
 }
 
-template <int BN, int ACT>
+template <int BN, int ACT, bool SC = false>
 int launch_v2(TcArgs a, cudaStream_t s) {
   using C = Cfg2<BN>;
+  constexpr int smem = SC ? C::SMEM_SC : C::SMEM;
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT, SC>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
   a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
@@ -857,7 +917,7 @@ int launch_v2(TcArgs a, cudaStream_t s) {
   int rc = launch_status("linear_3xtf32_panel");
   if (rc == GLINT_OK) {
     const int64_t grid = std::min<int64_t>(a.num_tiles, sm_count());
-    gemm_v2_kernel<BN, ACT><<<static_cast<unsigned>(grid), kThreads2, C::SMEM, s>>>(
+    gemm_v2_kernel<BN, ACT, SC><<<static_cast<unsigned>(grid), kThreads2, smem, s>>>(
         a, static_cast<const uint8_t*>(panel));
     rc = launch_status("linear_3xtf32");
   }
@@ -883,9 +943,52 @@ int launch_v2_bn(const TcArgs& a, int act, cudaStream_t s) {
   return launch_v2_act<128>(a, act, s);
 }
 
+// GAT projection with fused scores: needs every head inside one n-tile.
+int launch_v2_scores(const TcArgs& a, cudaStream_t s) {
+  const int nt = static_cast<int>(ceil_div(a.N, 128));
+  const int per = static_cast<int>(ceil_div(a.N, nt));
+  auto fits = [&](int bn) { return ceil_div(a.N, bn) == 1 || bn % a.head_pitch == 0; };
+  if (per <= 32 && fits(32)) return launch_v2<32, GLINT_ACT_NONE, true>(a, s);
+  if (per <= 48 && fits(48)) return launch_v2<48, GLINT_ACT_NONE, true>(a, s);
+  if (per <= 64 && fits(64)) return launch_v2<64, GLINT_ACT_NONE, true>(a, s);
+  if (per <= 96 && fits(96)) return launch_v2<96, GLINT_ACT_NONE, true>(a, s);
+  if (fits(128)) return launch_v2<128, GLINT_ACT_NONE, true>(a, s);
+  return GLINT_EUNSUPPORTED;
+}
+
 }  // namespace v2
 
 }  // namespace
+
+// Z = A W_pad^T (3xTF32) with s_src / s_dst computed in the epilogue; returns
+// GLINT_EUNSUPPORTED when the shape does not fit (the caller falls back).
+int launch_gat_project_3xtf32(int64_t M, int heads, int head_dim, int head_pitch, int K,
+                              const float* A, int64_t lda, const int64_t* a_rows, const float* W,
+                              int64_t ldw, const float* attn, float* Z, int64_t ldz, float* s_src,
+                              float* s_dst, cudaStream_t s) {
+  const int N = heads * head_pitch;
+  const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
+  if (!vec || N > v2::kScMaxN || tuning(GLINT_TUNE_GEMM_V1) != 0) return GLINT_EUNSUPPORTED;
+  TcArgs a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.A = A;
+  a.lda = lda;
+  a.a_rows = a_rows;
+  a.W = W;
+  a.ldw = ldw;
+  a.C = Z;
+  a.ldc = ldz;
+  a.c_vec4 = (ldz % 4 == 0) && aligned16(Z);
+  a.attn = attn;
+  a.s_src = s_src;
+  a.s_dst = s_dst;
+  a.heads = heads;
+  a.head_dim = head_dim;
+  a.head_pitch = head_pitch;
+  return v2::launch_v2_scores(a, s);
+}
 
 int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
                          const int64_t* a_rows, const float* W, int64_t ldw, const float* bias,

@@ -16,6 +16,10 @@ namespace glint {
 int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
                          const int64_t* a_rows, const float* W, int64_t ldw, const float* bias,
                          int act, float* C, int64_t ldc, cudaStream_t s);
+int launch_gat_project_3xtf32(int64_t M, int heads, int head_dim, int head_pitch, int K,
+                              const float* A, int64_t lda, const int64_t* a_rows, const float* W,
+                              int64_t ldw, const float* attn, float* Z, int64_t ldz, float* s_src,
+                              float* s_dst, cudaStream_t s);
 
 namespace {
 
@@ -180,6 +184,29 @@ int glint_gat_scores_f32(int64_t M, int32_t heads, int32_t head_dim, int32_t hea
   gat_scores_kernel<<<static_cast<unsigned>(grid), 256, 0, as_stream(stream)>>>(
       M, heads, head_dim, head_pitch, Z, ldz, attn, s_src, s_dst);
   return launch_status("gat_scores");
+}
+
+int glint_gat_project_f32(int64_t M, int32_t heads, int32_t head_dim, int32_t head_pitch,
+                          int32_t K, const float* A, int64_t lda, const int64_t* a_rows,
+                          const float* W_pad, int64_t ldw, const float* attn, float* Z,
+                          int64_t ldz, float* s_src, float* s_dst, int32_t precision,
+                          glint_stream_t stream) {
+  GLINT_REQUIRE(M >= 0 && heads >= 1 && head_dim >= 1 && head_pitch >= head_dim && K >= 1,
+                "gat_project: bad shape");
+  if (M == 0) return GLINT_OK;
+  GLINT_REQUIRE(A && W_pad && attn && Z && s_src && s_dst, "gat_project: null argument");
+  const int N = heads * head_pitch;
+  GLINT_REQUIRE(lda >= K && ldw >= K && ldz >= N, "gat_project: leading dimension too small");
+  cudaStream_t s = as_stream(stream);
+  if (precision == GLINT_PREC_3XTF32) {
+    const int rc = launch_gat_project_3xtf32(M, heads, head_dim, head_pitch, K, A, lda, a_rows,
+                                             W_pad, ldw, attn, Z, ldz, s_src, s_dst, s);
+    if (rc != GLINT_EUNSUPPORTED) return rc;
+  }
+  const int rc = glint_linear_f32(M, N, K, A, lda, a_rows, W_pad, ldw, nullptr, GLINT_ACT_NONE, Z,
+                                  ldz, precision, stream);
+  if (rc) return rc;
+  return glint_gat_scores_f32(M, heads, head_dim, head_pitch, Z, ldz, attn, s_src, s_dst, stream);
 }
 
 }  // extern "C"

@@ -407,12 +407,13 @@ def attn_project(h, w_pad, attn, heads, head_dim, precision=None):
     hp = head_pitch(head_dim)
     M = h.shape[0]
     Z = torch.empty((M, heads * hp), dtype=torch.float32, device=h.device)
-    linear_into(Z, h, w_pad, None, _lib.ACT_NONE, precision=precision)
     s_src = torch.empty((M, heads), dtype=torch.float32, device=h.device)
     s_dst = torch.empty((M, heads), dtype=torch.float32, device=h.device)
     a = _f32(attn).contiguous()
-    _lib.call("glint_gat_scores_f32", M, heads, head_dim, hp, ptr(Z), ld(Z), ptr(a), ptr(s_src),
-              ptr(s_dst), stream_handle())
+    prec = PRECISION if precision is None else precision
+    _lib.call("glint_gat_project_f32", M, heads, head_dim, hp, int(w_pad.shape[1]), ptr(h), ld(h),
+              None, ptr(w_pad), ld(w_pad), ptr(a), ptr(Z), ld(Z), ptr(s_src), ptr(s_dst),
+              int(prec), stream_handle())
     return Z, s_src, s_dst
 
 
