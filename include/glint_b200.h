@@ -74,6 +74,7 @@ int glint_abi_version(void);
 #define GLINT_TUNE_GAT_VARIANT 3  /* K4 launch variant (occupancy / unroll) */
 #define GLINT_TUNE_GEMM_V1 4      /* 1: K2 uses the single-accumulator tcgen05 kernel */
 #define GLINT_TUNE_GEMM_RAWHI 5   /* experiment: unmasked fp32 as the tf32 "hi" operand */
+#define GLINT_TUNE_HUB_CTAS_PER_SM 6 /* K1 register hub kernel: k > 0 caps it at k CTAs per SM */
 #define GLINT_TUNE_COUNT 8
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);

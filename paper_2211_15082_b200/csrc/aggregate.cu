@@ -217,12 +217,17 @@ __device__ __forceinline__ void mean_row_hub(const MeanArgs& a, int64_t r, int c
   }
 }
 
-// Hub rows, register path: one 256-thread CTA per (hub row, 256 columns).
+// Hub rows, register path: a 256-thread CTA per (hub row, 256 columns) unit.
+// Persistent grid (units strided over the CTAs, longest rows first): launched
+// with about one CTA per SM it runs beside the concurrent regular-row kernel
+// instead of filling every SM with hub CTAs ahead of it.
 __global__ void __launch_bounds__(kThreads) mean_hub_reg_kernel(MeanArgs a) {
   __shared__ int64_t s_off[kHubChunk];
-  const int64_t hub = blockIdx.x / a.sc.hub_col_blocks;
-  const int cb = static_cast<int>(blockIdx.x % a.sc.hub_col_blocks);
-  mean_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off);
+  for (int64_t unit = blockIdx.x; unit < a.sc.hub_ctas; unit += gridDim.x) {
+    const int64_t hub = unit / a.sc.hub_col_blocks;
+    const int cb = static_cast<int>(unit % a.sc.hub_col_blocks);
+    mean_row_hub(a, static_cast<int64_t>(a.sc.schedule[hub]), cb, s_off);
+  }
 }
 
 // Regular rows (schedule entries n_hub..n_rows): LPR lanes per row.  Hub rows
@@ -697,7 +702,13 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
   } else if (vec4 && (knob >= 2 || (knob == 0 && a.sc.n_rows < (1 << 19)))) {
     rc = launch_hub(a, ss->stream);
   } else {
-    mean_hub_reg_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
+    // CTAs per SM for the register hub kernel: knob 6 = k caps the grid at
+    // k CTAs per SM (persistent); 0 (default) = one CTA per unit, measured
+    // best (profiles/r01_spmm_sweep_hub.jsonl: d=48 4.06 ms vs 4.85 at 1/SM)
+    const int per_sm = tuning(GLINT_TUNE_HUB_CTAS_PER_SM);
+    const int64_t cap = per_sm == 0 ? a.sc.hub_ctas : static_cast<int64_t>(per_sm) * sm_count();
+    const int64_t grid = std::min<int64_t>(a.sc.hub_ctas, cap);
+    mean_hub_reg_kernel<<<static_cast<unsigned>(grid), kThreads, 0, ss->stream>>>(a);
     rc = launch_status("spmm_mean_hub");
   }
   if (rc) return rc;

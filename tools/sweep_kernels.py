@@ -129,6 +129,15 @@ def main():
                                   "GBps": agg_bytes(d, e_r, size) / ms / 1e6}), flush=True)
             _lib.call("glint_set_tuning", 2, 0)
             pos += size
+        # register hub kernel: k CTAs per SM, persistent (0 = one CTA per hub unit)
+        for per_sm in (1, 2, 4, 0):
+            _lib.call("glint_set_tuning", 6, per_sm)
+            ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n, schedule=sched,
+                                                 n_hub=hub_pre), args.reps)
+            print(json.dumps({"kernel": "spmm_mean_hub_per_sm", "dim": d, "per_sm": per_sm,
+                              "ms": ms, "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
+                              "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+        _lib.call("glint_set_tuning", 6, 0)
         # natural order, no hub path (effect of the LPT schedule)
         _lib.call("glint_set_tuning", 0, 0)
         ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n))
