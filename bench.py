@@ -361,8 +361,14 @@ def main():
         "kernel": agg_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
         "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
         "traffic": traffic_from_profiles(agg_name),
+        "traffic_basis": "DRAM read+write bytes per aggregation launch (regular + hub kernels), "
+                         "ncu launch list of this bench step (profiles/ncu_traffic.json); "
+                         "compare with algorithmic_bytes_per_launch",
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+        "achieved_basis": "sum of SURVEY 8d B_agg over the step's aggregation launches / sum of "
+                          "their CUDA-event durations (same stream)",
         "launches_per_step": cnt // max(args.steps, 1),
+        "algorithmic_bytes_per_launch": nbytes // max(cnt, 1),
         "algorithmic_bytes_per_step": nbytes // max(args.steps, 1),
         "kernel_ms_per_step": agg_ms / max(args.steps, 1),
         "kernel_share_of_step": (agg_ms / args.steps) / ms if ms else None,

@@ -126,18 +126,59 @@ def main():
             md.append(f"| {short(n)} | {c} | {s:.3f} | {100 * s / total:.1f}% |")
     prefix.with_suffix(".json").write_text(json.dumps(out, indent=1) + "\n")
     prefix.with_suffix(".md").write_text("\n".join(md) + "\n")
-    traffic_path = ROOT / "profiles" / "ncu_traffic.json"
-    traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
-    for key, stem in (("spmm_mean", "mean_kernel"), ("gat_aggregate", "gat_kernel")):
-        hits = [r for r in recs if stem in r["kernel"]]
-        if not hits:
-            continue
-        dram = sum(r.get("dram_read_bytes", 0) + r.get("dram_write_bytes", 0) for r in hits)
-        traffic[key] = {"dram_bytes_per_launch": dram / len(hits), "launches": len(hits),
-                        "dram_bytes_total": dram, "reports": sorted({r["report"] for r in hits}),
-                        "duration_ms_total": sum(r.get("duration_ms", 0) for r in hits)}
-    traffic_path.write_text(json.dumps(traffic, indent=1) + "\n")
+    if lfile:
+        step = step_traffic(lfile)
+        if step:
+            traffic_path = ROOT / "profiles" / "ncu_traffic.json"
+            traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
+            traffic.update(step)
+            traffic_path.write_text(json.dumps(traffic, indent=1) + "\n")
+            out["step_traffic"] = step
+            prefix.with_suffix(".json").write_text(json.dumps(out, indent=1) + "\n")
     print("\n".join(md))
+
+
+# K1 / K4 calls: the regular-row kernel plus its concurrent hub-row kernel
+FAMILIES = {"spmm_mean": ("mean_async_kernel", "mean_kernel<", "mean_hub"),
+            "gat_aggregate": ("gat_kernel<", "gat_async_kernel", "gat_hub")}
+
+
+def step_traffic(lfile):
+    """DRAM bytes per aggregation call of the LAST bench step in a launch list
+    captured with dram__bytes_{read,write}.sum (bench.py --steps 1 --warmup 1:
+    the second half of the calls).  A call = its regular-row launch (+ hub launch)."""
+    rows = list(csv.reader(open(lfile)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"]
+    if not hi:
+        return {}
+    h = rows[hi[0]]
+    ii, ki, mi, vi = (h.index(x) for x in ("ID", "Kernel Name", "Metric Name", "Metric Value"))
+    per = {}
+    for r in rows[hi[0] + 1:]:
+        if len(r) <= vi:
+            continue
+        d = per.setdefault(int(r[ii]), {"kernel": r[ki]})
+        try:
+            d[r[mi]] = float(r[vi].replace(",", ""))
+        except ValueError:
+            pass
+    launches = [per[k] for k in sorted(per)]
+    res = {}
+    for key, stems in FAMILIES.items():
+        fam = [x for x in launches if any(s in x["kernel"] for s in stems)]
+        regular = [x for x in fam if "hub" not in x["kernel"]]
+        if not regular or "dram__bytes_read.sum" not in regular[0]:
+            continue
+        calls = len(regular) // 2
+        first = fam.index(regular[calls])          # first regular launch of the last step
+        last = fam[first - 1] if first and "hub" in fam[first - 1]["kernel"] else None
+        step = ([last] if last else []) + fam[first:]
+        dram = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in step)
+        res[key] = {"dram_bytes_per_launch": dram / calls, "launches": calls,
+                    "dram_bytes_per_step": dram, "source": pathlib.Path(lfile).name,
+                    "basis": "ncu launch list (gpu__time_duration, dram__bytes_*), last bench "
+                             "step; a launch = one aggregation call (regular + hub kernels)"}
+    return res
 
 
 if __name__ == "__main__":
