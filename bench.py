@@ -74,10 +74,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GLINT_DIST_BACKEND=gloo runs several ranks on one GPU (NCCL refuses
+    # duplicate devices): a functional check of the multi-rank path on a
+    # 1-GPU box, not a performance configuration.
+    backend = os.environ.get("GLINT_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
     if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
     return rank, world, local
 
 

@@ -174,3 +174,26 @@ def test_nodewise_hard_oom(golden, cuda):
     with pytest.raises(DeviceCapacityError):
         run_inference(build_gcn(3, 4, 2, 2, seed=2), toy, gen_features(6, 3, 0),
                       executor="nodewise", budget=DeviceBudget(64), batch_size=6)
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
+    """The torchrun path (edge-balanced row ranges + per-layer exchange) gives the
+    single-rank bytes for GCN and GAT, one batch and many batches per layer.
+    Two ranks share cuda:0 over gloo (NCCL refuses duplicate devices)."""
+    import json
+    import os
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    env = dict(os.environ, GLINT_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533",
+           str(root / "tools" / "dist_check.py"), "20000"]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 4
+    assert all(x["bit_identical_all_ranks"] for x in lines), lines
