@@ -363,11 +363,12 @@ class LayerwiseEngine:
 
     def __init__(self, m: ModelGraph, schedule: BlockSchedule, g: DeviceGraph, x: DeviceStore,
                  tsets: TargetSets, budget, thresholds: Thresholds, stats: RunStats,
-                 precision=None, row_range=None, reassociate=True):
+                 precision=None, row_range=None, reassociate=True, release_input=False):
         import torch
 
         self.m, self.schedule, self.g, self.tsets = m, schedule, g, tsets
         self.reassociate = reassociate
+        self.release_input = release_input  # engine owns x: free it after its last reader
         self.budget, self.stats = budget, stats
         self.controller = BatchController(thresholds=thresholds, budget=budget)
         self.dev = g.indptr.device
@@ -851,8 +852,9 @@ class LayerwiseEngine:
 
     def release_after(self, blk):
         out_key = self.schedule.model_output.key
+        keep = (out_key,) if self.release_input else (INPUT_REF, out_key)
         for key, last in self.schedule.drop_after.items():
-            if last == blk.block_id and key not in (INPUT_REF, out_key):
+            if last == blk.block_id and key not in keep:
                 st = self.stores.pop(key, None)
                 if st is not None:
                     st.release()
@@ -1306,6 +1308,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         if probe is not None:
             probe.mark("output streamed (copy stream)", streamed.stream)
         output_val = streamed.finish()
+        if probe is not None:
+            probe.mark("output on host")
     elif host_out:
         staging = torch.empty(tuple(out_dev.shape), dtype=torch.float32, pin_memory=True)
         staging.copy_(out_dev)
@@ -1314,6 +1318,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         output_val = out_dev
     torch.cuda.synchronize(dg0.device)
     stats.wall_time = time.perf_counter() - started
+    if probe is not None:
+        probe.mark("return")
     return InferenceResult(output=output_val, target_ids=user_targets, stats=stats,
                            order=node_order, schedule=schedule, budget=bud)
 
