@@ -51,9 +51,6 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--model", choices=["gcn3", "gat3"], default="gcn3")
-    p.add_argument("--graph", choices=["products", "papers"], default="products",
-                   help="products: cfg2/cfg3 (default); papers: cfg5, Papers100M-shaped "
-                        "(111M nodes, 1.6B edges, 3-layer GCN 128->128->128->172)")
     p.add_argument("--nodes", type=int, default=None)
     p.add_argument("--undirected", type=int, default=None)
     p.add_argument("--precision", choices=["fp32", "3xtf32"], default=None)
@@ -110,14 +107,6 @@ def max_over_ranks(x, world):
 def workload(args):
     from paper_2211_15082_b200 import synth
 
-    if args.graph == "papers":
-        n = args.nodes or synth.PAPERS_NODES
-        und = args.undirected or (synth.PAPERS_EDGES // 2 if args.nodes is None
-                                  else int(round(n * synth.PAPERS_EDGES / 2 / synth.PAPERS_NODES)))
-        if args.model != "gcn3":
-            raise SystemExit("--graph papers runs the cfg5 GCN only")
-        return n, und, synth.build_gcn(128, 128, 172, 3, seed=0), \
-            "3-layer GCN (ConvMean 128->128->128->172, ReLU)"
     n = args.nodes or synth.PRODUCTS_NODES
     und = args.undirected or (synth.PRODUCTS_UNDIRECTED if args.nodes is None
                               else int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES)))
@@ -280,11 +269,11 @@ def run_reference(args, rank, world):
 
 
 def config_block(args, n, und, desc, world):
-    papers = args.graph == "papers"
-    cfg = "cfg5" if papers else ("cfg2" if args.model == "gcn3" else "cfg3")
-    shape = "OGBN-Papers100M-shaped" if papers else "OGBN-Products-shaped"
-    din, dh = (128, 128) if papers else (100, 256)
-    return {"workload": f"{cfg} {desc} full inference, {shape} graph",
+    # cfg5 (Papers100M-shaped, 1.6B edges) runs in tools/bench_papers.py: its
+    # features cannot stay resident next to the layer-3 output on one GPU.
+    cfg = "cfg2" if args.model == "gcn3" else "cfg3"
+    din, dh = 100, 256
+    return {"workload": f"{cfg} {desc} full inference, OGBN-Products-shaped graph",
             "nodes": n, "in_edges": 2 * und, "model": args.model, "mode": "full",
             "order": "none", "budget": "device (free HBM after resident stores)",
             "l2": "inputs larger than L2 (features %.2f GB, hidden %.2f GB per layer)"
