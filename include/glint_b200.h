@@ -265,6 +265,12 @@ int glint_narrow_ids(int64_t n, const int64_t* src, int32_t* dst,
  * reference's tie rules (reorder.py:55-123). perm_out[new] = old. */
 int glint_rcmk_host(int64_t num_nodes, const int64_t* indptr,
                     const int64_t* indices, int64_t* perm_out);
+/* The same order from a symmetrised adjacency whose rows are already
+ * deduplicated, free of self loops and ordered by (degree, id) -- built on the
+ * device by reorder._sorted_adjacency_device -- so the host pass is linear
+ * (components, then BFS).  Host pointers. */
+int glint_rcmk_sorted_host(int64_t num_nodes, const int64_t* ptr,
+                           const int32_t* adj, int64_t* perm_out);
 
 #ifdef __cplusplus
 }

@@ -117,3 +117,64 @@ extern "C" int glint_rcmk_host(int64_t n, const int64_t* indptr, const int64_t* 
   for (int64_t i = 0; i < n; ++i) perm_out[i] = seq[n - 1 - i];
   return GLINT_OK;
 }
+
+// Same ordering from a pre-sorted symmetrised adjacency: row v of (ptr, adj)
+// holds v's distinct neighbours (self loops dropped) already ordered by
+// (degree, id), degree = ptr[v+1] - ptr[v].  The device builds it (two sorts,
+// reorder.py _sorted_adjacency_device), so the host pass is two linear sweeps:
+// components in seed order (start = min (degree, id) member, components in
+// ascending start order), then the BFS, whose per-node candidate list is the
+// row filtered by `visited` -- the (degree, id) order is preserved by the
+// filter, so no per-node sort remains.
+extern "C" int glint_rcmk_sorted_host(int64_t n, const int64_t* ptr, const int32_t* adj,
+                                      int64_t* perm_out) {
+  if (n < 0 || (n > 0 && (!ptr || !perm_out))) return GLINT_EINVAL;
+  if (n == 0) return GLINT_OK;
+  auto deg = [&](int64_t v) { return ptr[v + 1] - ptr[v]; };
+  std::vector<int32_t> comp(n, -1);
+  std::vector<int64_t> starts;
+  std::vector<int64_t> stack;
+  for (int64_t seed = 0; seed < n; ++seed) {
+    if (comp[seed] >= 0) continue;
+    const int32_t c = static_cast<int32_t>(starts.size());
+    int64_t best = seed;
+    comp[seed] = c;
+    stack.push_back(seed);
+    while (!stack.empty()) {
+      const int64_t u = stack.back();
+      stack.pop_back();
+      if (deg(u) < deg(best) || (deg(u) == deg(best) && u < best)) best = u;
+      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+        const int64_t v = adj[e];
+        if (v < 0 || v >= n) return GLINT_EINVAL;
+        if (comp[v] < 0) {
+          comp[v] = c;
+          stack.push_back(v);
+        }
+      }
+    }
+    starts.push_back(best);
+  }
+  std::sort(starts.begin(), starts.end());
+  std::vector<char> visited(n, 0);
+  std::vector<int64_t> seq(n);
+  int64_t pos = 0;
+  for (int64_t s : starts) {
+    seq[pos] = s;
+    visited[s] = 1;
+    int64_t head = pos++;
+    while (head < pos) {
+      const int64_t u = seq[head++];
+      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+        const int64_t v = adj[e];
+        if (!visited[v]) {
+          visited[v] = 1;
+          seq[pos++] = v;
+        }
+      }
+    }
+  }
+  if (pos != n) return GLINT_ECUDA;  // internal invariant
+  for (int64_t i = 0; i < n; ++i) perm_out[i] = seq[n - 1 - i];
+  return GLINT_OK;
+}

@@ -82,8 +82,57 @@ def _host_csc(g):
     return g.indptr_host, g.indices.cpu().numpy().astype(np.int64)
 
 
+def _sorted_adjacency_device(dg):
+    """Symmetrised adjacency of a DeviceGraph with every row deduplicated, free
+    of self loops and ordered by (degree, id) -- the order the RCMK BFS visits
+    candidates in (reorder.py:89-99).  Two device sorts: (row, col) to merge
+    duplicates and count degrees, then (row, rank of col by (degree, id)).
+    Returns host (ptr int64 [n+1], adj int32 [nnz])."""
+    import torch
+
+    n = int(dg.num_nodes)
+    dev = dg.indptr.device
+    deg_in = dg.indptr[1:] - dg.indptr[:-1]
+    dst = torch.repeat_interleave(torch.arange(n, device=dev), deg_in)
+    src = dg.indices.to(torch.int64)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    key = torch.unique(torch.cat([src * n + dst, dst * n + src]))   # sorted, deduplicated
+    del src, dst, keep
+    row = key // n
+    col = key - row * n
+    del key
+    deg = torch.bincount(row, minlength=n)
+    order = torch.sort(deg * n + torch.arange(n, device=dev)).indices     # by (degree, id)
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(n, device=dev)
+    key2 = torch.sort(row * n + rank[col]).values
+    del row, col
+    adj = order[key2 % n].to(torch.int32)
+    ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(deg, 0, out=ptr[1:])
+    return ptr.cpu().numpy(), adj.cpu().numpy()
+
+
 def rcmk(g) -> NodeOrder:
-    """Reverse Cuthill-McKee over in- plus out-edges (native C++)."""
+    """Reverse Cuthill-McKee over in- plus out-edges.
+
+    A DeviceGraph gets its (degree, id)-sorted symmetric adjacency built on the
+    device and a linear native BFS; a host CscGraph runs the all-host native
+    version (same tie rules, same permutation).
+    """
+    from .storage import DeviceGraph
+
+    if isinstance(g, DeviceGraph) and int(g.num_nodes) > 0:
+        ptr, adj = _sorted_adjacency_device(g)
+        n = int(g.num_nodes)
+        perm = np.empty(n, dtype=np.int64)
+        rc = _lib.load().glint_rcmk_sorted_host(n, ptr.ctypes.data_as(ctypes.c_void_p),
+                                                adj.ctypes.data_as(ctypes.c_void_p),
+                                                perm.ctypes.data_as(ctypes.c_void_p))
+        if rc != 0:
+            raise ValueError(f"rcmk failed with status {rc}")
+        return NodeOrder(perm)
     indptr, indices = _host_csc(g)
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     indices = np.ascontiguousarray(indices, dtype=np.int64)
