@@ -261,6 +261,24 @@ int glint_relabel_csc(int64_t num_nodes, const int64_t* old_indptr,
 int glint_narrow_ids(int64_t n, const int64_t* src, int32_t* dst,
                      int64_t limit, int64_t* bad_out, glint_stream_t stream);
 
+/* ---------------------------------------------------- neighbour sampling
+ * Replaces executor.py:74-115 sample_neighbors on the device.  For selected
+ * node i (id nodes[i], or i when nodes is NULL): its in-edge slots s get
+ * prio = mix(base ^ mix(v*M1) ^ s), base = mix(mix(seed) ^ mix(layer*M2))
+ * (splitmix64), it keeps its min(fanout, deg) smallest priorities (ties by
+ * slot) and writes the kept source ids ascending to
+ * out_indices[out_off[i] .. out_off[i+1]).  local_off[i] = sum of deg over
+ * selected nodes before i (n_sel+1 entries, e_sel = local_off[n_sel]).
+ * All arrays device memory; scratch from glint_sample_workspace_bytes. */
+size_t glint_sample_workspace_bytes(int64_t n_sel, int64_t e_sel, int64_t e_out);
+int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices,
+                           const int64_t* nodes, int64_t n_sel,
+                           const int64_t* local_off, int64_t e_sel,
+                           const int64_t* out_off, int64_t e_out, int32_t fanout,
+                           int64_t seed, int32_t layer, int32_t* out_indices,
+                           void* workspace, size_t workspace_bytes,
+                           glint_stream_t stream);
+
 /* Host-side (pure C++, host pointers): reverse Cuthill-McKee order with the
  * reference's tie rules (reorder.py:55-123). perm_out[new] = old. */
 int glint_rcmk_host(int64_t num_nodes, const int64_t* indptr,

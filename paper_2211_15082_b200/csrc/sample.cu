@@ -1,0 +1,152 @@
+// Neighbour sampling on the device (reference: executor.py:74-115
+// sample_neighbors).  Every in-edge slot s of a selected node v gets the
+// priority
+//   prio = mix(base ^ mix(v * M1) ^ s),  base = mix(mix(seed) ^ mix(layer * M2))
+// (splitmix64 finaliser, wrapping uint64 arithmetic).  The node keeps its
+// min(fanout, deg) smallest priorities -- ties by slot, as numpy's stable
+// lexsort -- and the kept sources are stored ascending.
+//
+// Device pipeline (all on the caller's stream, scratch in the caller's
+// workspace):
+//   1. prio_kernel: one warp per selected node writes (prio, source) for its
+//      slots into the node's segment;
+//   2. cub::DeviceSegmentedSort::StableSortPairs by priority per segment
+//      (stable: equal priorities keep slot order);
+//   3. keep_kernel: the first min(fanout, deg) sources of each segment;
+//   4. cub::DeviceSegmentedSort::SortKeys per output segment (ascending ids).
+#include <cub/device/device_segmented_sort.cuh>
+
+#include "common.cuh"
+
+namespace glint {
+namespace {
+
+constexpr uint64_t kM1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kM2 = 0x94D049BB133111EBull;
+constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = x + kGold;
+  z = (z ^ (z >> 30)) * kM1;
+  z = (z ^ (z >> 27)) * kM2;
+  return z ^ (z >> 31);
+}
+
+__global__ void prio_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
+                            const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int64_t* __restrict__ local_off, uint64_t base,
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_sel) return;
+  const int64_t v = nodes ? nodes[w] : w;
+  const int64_t beg = indptr[v];
+  const int64_t deg = indptr[v + 1] - beg;
+  const int64_t out = local_off[w];
+  const uint64_t hv = base ^ mix64(static_cast<uint64_t>(v) * kM1);
+  for (int64_t s = lane; s < deg; s += 32) {
+    keys[out + s] = mix64(hv ^ static_cast<uint64_t>(s));
+    vals[out + s] = indices[beg + s];
+  }
+}
+
+__global__ void keep_kernel(int64_t n_sel, const int64_t* __restrict__ local_off,
+                            const int64_t* __restrict__ out_off, const int32_t* __restrict__ sorted,
+                            int32_t* __restrict__ kept) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_sel) return;
+  const int64_t src = local_off[w];
+  const int64_t dst = out_off[w];
+  const int64_t cnt = out_off[w + 1] - dst;
+  for (int64_t j = lane; j < cnt; j += 32) kept[dst + j] = sorted[src + j];
+}
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+struct SampleWs {
+  size_t keys, vals, kept, temp, total;
+};
+
+int sample_ws(int64_t n_sel, int64_t e_sel, int64_t e_out, SampleWs* ws) {
+  size_t t1 = 0, t2 = 0;
+  GLINT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+      nullptr, t1, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
+      static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), static_cast<int>(e_sel),
+      static_cast<int>(n_sel), static_cast<const int64_t*>(nullptr),
+      static_cast<const int64_t*>(nullptr)));
+  GLINT_CUDA(cub::DeviceSegmentedSort::SortKeys(
+      nullptr, t2, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+      static_cast<int>(e_out), static_cast<int>(n_sel), static_cast<const int64_t*>(nullptr),
+      static_cast<const int64_t*>(nullptr)));
+  ws->keys = align256(2 * sizeof(uint64_t) * static_cast<size_t>(e_sel));
+  ws->vals = align256(2 * sizeof(int32_t) * static_cast<size_t>(e_sel));
+  ws->kept = align256(sizeof(int32_t) * static_cast<size_t>(e_out));
+  ws->temp = align256(std::max(t1, t2));
+  ws->total = ws->keys + ws->vals + ws->kept + ws->temp;
+  return GLINT_OK;
+}
+
+}  // namespace
+}  // namespace glint
+
+using namespace glint;
+
+extern "C" {
+
+size_t glint_sample_workspace_bytes(int64_t n_sel, int64_t e_sel, int64_t e_out) {
+  if (n_sel < 0 || e_sel < 0 || e_out < 0 || e_sel >= (1LL << 31) || n_sel >= (1LL << 31))
+    return 0;
+  SampleWs ws{};
+  if (sample_ws(n_sel, e_sel, e_out, &ws) != GLINT_OK) return 0;
+  return ws.total;
+}
+
+int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices, const int64_t* nodes,
+                           int64_t n_sel, const int64_t* local_off, int64_t e_sel,
+                           const int64_t* out_off, int64_t e_out, int32_t fanout, int64_t seed,
+                           int32_t layer, int32_t* out_indices, void* workspace,
+                           size_t workspace_bytes, glint_stream_t stream) {
+  GLINT_REQUIRE(fanout >= 1, "sample_neighbors: fanout must be >= 1, got %d", fanout);
+  GLINT_REQUIRE(n_sel >= 0 && e_sel >= 0 && e_out >= 0 && e_out <= e_sel,
+                "sample_neighbors: bad sizes");
+  GLINT_REQUIRE(e_sel < (1LL << 31) && n_sel < (1LL << 31),
+                "sample_neighbors: more than 2^31 edges or nodes per call");
+  if (n_sel == 0 || e_sel == 0) return GLINT_OK;
+  GLINT_REQUIRE(indptr && indices && local_off && out_off && out_indices && workspace,
+                "sample_neighbors: null argument");
+  SampleWs ws{};
+  int rc = sample_ws(n_sel, e_sel, e_out, &ws);
+  if (rc) return rc;
+  GLINT_REQUIRE(workspace_bytes >= ws.total, "sample_neighbors: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  uint8_t* p = static_cast<uint8_t*>(workspace);
+  uint64_t* keys_in = reinterpret_cast<uint64_t*>(p);
+  uint64_t* keys_out = keys_in + e_sel;
+  int32_t* vals_in = reinterpret_cast<int32_t*>(p + ws.keys);
+  int32_t* vals_out = vals_in + e_sel;
+  int32_t* kept = reinterpret_cast<int32_t*>(p + ws.keys + ws.vals);
+  void* temp = p + ws.keys + ws.vals + ws.kept;
+  const uint64_t base = mix64(mix64(static_cast<uint64_t>(seed)) ^
+                              mix64(static_cast<uint64_t>(static_cast<int64_t>(layer)) * kM2));
+  const int64_t blocks = ceil_div(n_sel * 32, 256);
+  prio_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n_sel, nodes, indptr, indices,
+                                                             local_off, base, keys_in, vals_in);
+  rc = launch_status("sample_prio");
+  if (rc) return rc;
+  size_t tb = ws.temp;
+  GLINT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+      temp, tb, keys_in, keys_out, vals_in, vals_out, static_cast<int>(e_sel),
+      static_cast<int>(n_sel), local_off, local_off + 1, s));
+  keep_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n_sel, local_off, out_off, vals_out,
+                                                             kept);
+  rc = launch_status("sample_keep");
+  if (rc) return rc;
+  tb = ws.temp;
+  GLINT_CUDA(cub::DeviceSegmentedSort::SortKeys(temp, tb, kept, out_indices,
+                                                static_cast<int>(e_out), static_cast<int>(n_sel),
+                                                out_off, out_off + 1, s));
+  return launch_status("sample_sort");
+}
+
+}  // extern "C"

@@ -74,8 +74,11 @@ def _mix(x):
     return z ^ (z >> _U64(31))
 
 
-def sample_neighbors(g, nodes, fanout, seed, layer) -> CscGraph:
+def sample_neighbors(g, nodes, fanout, seed, layer):
     """min(fanout, deg) distinct in-neighbours per node (glint/executor.py:74-115).
+
+    A DeviceGraph is sampled on the device and returns a DeviceGraph; a host
+    CscGraph keeps the numpy path (the oracle-pinned restatement).
 
     Edge priority = mix(base ^ mix(node * M1) ^ slot), base = mix(mix(seed) ^
     mix(layer * M2)); each node keeps its `fanout` smallest priorities and the
@@ -84,6 +87,11 @@ def sample_neighbors(g, nodes, fanout, seed, layer) -> CscGraph:
     """
     if fanout < 1:
         raise ValueError(f"fanout must be >= 1, got {fanout}")
+    if isinstance(g, DeviceGraph):
+        # device draws (glint_sample_neighbors): same priorities, same bytes
+        nodes = np.unique(np.asarray(nodes, dtype=np.int64))
+        every = len(nodes) == g.num_nodes
+        return kernels.sample_neighbors_dev(g, None if every else nodes, fanout, seed, layer)
     indptr_h, indices_h = _host_arrays(g)
     n = g.num_nodes
     nodes = np.unique(np.asarray(nodes, dtype=np.int64))

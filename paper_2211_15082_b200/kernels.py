@@ -241,6 +241,54 @@ def degree_schedule(indptr, row_ids=None, row_base=0, n_rows=0, hub_min=None):
     return sched, n_hub
 
 
+def sample_neighbors_dev(dg, nodes, fanout, seed, layer):
+    """Device neighbour sampling (glint/executor.py:74-115) -> DeviceGraph.
+
+    nodes: sorted unique host int64 ids (or None = every node).  The segment
+    offsets come from the host indptr (no device sync); draws, selection and
+    the ascending sort of each kept slice run in glint_sample_neighbors.
+    """
+    import numpy as np
+
+    from .storage import DeviceGraph
+
+    torch = _torch()
+    n = int(dg.num_nodes)
+    ip_h = np.asarray(dg.indptr_host, dtype=np.int64)
+    degs_all = np.diff(ip_h)
+    if nodes is None:
+        degs = degs_all
+        nodes_dev = None
+    else:
+        nodes = np.asarray(nodes, dtype=np.int64)
+        degs = degs_all[nodes]
+        nodes_dev = torch.from_numpy(nodes).to(dg.indptr.device)
+    kept = np.minimum(degs, int(fanout))
+    local_off = np.zeros(len(degs) + 1, dtype=np.int64)
+    np.cumsum(degs, out=local_off[1:])
+    out_off = np.zeros(len(degs) + 1, dtype=np.int64)
+    np.cumsum(kept, out=out_off[1:])
+    e_sel, e_out = int(local_off[-1]), int(out_off[-1])
+    full_ptr = np.zeros(n + 1, dtype=np.int64)
+    if nodes is None:
+        full_ptr[1:] = kept
+    else:
+        full_ptr[nodes + 1] = kept
+    np.cumsum(full_ptr, out=full_ptr)
+    dev = dg.indptr.device
+    out_idx = torch.empty(max(e_out, 1), dtype=torch.int32, device=dev)[:e_out]
+    if e_out:
+        dg.wait_rows()
+        lo = torch.from_numpy(local_off).to(dev)
+        oo = torch.from_numpy(out_off).to(dev)
+        wsb = _lib.query("glint_sample_workspace_bytes", len(degs), e_sel, e_out)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        _lib.call("glint_sample_neighbors", ptr(dg.indptr), ptr(dg.indices), ptr(nodes_dev),
+                  len(degs), ptr(lo), e_sel, ptr(oo), e_out, int(fanout), int(seed), int(layer),
+                  ptr(out_idx), ptr(ws), wsb, stream_handle())
+    return DeviceGraph(n, e_out, torch.from_numpy(full_ptr).to(dev), out_idx, full_ptr)
+
+
 # -------------------------------------------------------------- batch CSC --
 
 

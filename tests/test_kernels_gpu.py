@@ -387,3 +387,37 @@ def test_device_rcmk_matches_reference_and_host_path(golden, cuda):
         host = reorder.rcmk(g).perm
         dev = reorder.rcmk(kernels.device_graph(g)).perm
         assert np.array_equal(host, dev), (n, e)
+
+
+def test_device_sampling_matches_reference(golden, cuda):
+    """glint_sample_neighbors == the reference's draws (golden) and == the host
+    restatement on random graphs with duplicates, for all-node and subset draws."""
+    from paper_2211_15082_b200 import kernels
+    from paper_2211_15082_b200.executor import sample_neighbors
+    from paper_2211_15082_b200.storage import CscGraph
+
+    arrs, meta = golden
+    n_checked = 0
+    for c in meta["sampling"]:
+        g = golden_graph(arrs, c["graph"])
+        s = sample_neighbors(kernels.device_graph(g), np.arange(g.num_nodes), c["fanout"],
+                             c["seed"], c["layer"])
+        assert np.array_equal(np.asarray(s.indptr_host), arrs[c["indptr"]])
+        assert np.array_equal(s.indices.cpu().numpy().astype(np.int64), arrs[c["indices"]])
+        n_checked += 1
+    assert n_checked > 0
+    rng = np.random.default_rng(5)
+    for n, e, fanout in ((200, 3000, 5), (3000, 60000, 10), (1000, 20000, 1)):
+        dst = np.sort(rng.integers(0, n, size=e))
+        dst[:600] = 7                                       # one heavy row
+        dst = np.sort(dst)
+        src = rng.integers(0, n, size=e)
+        indptr = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+        g = CscGraph(n, e, indptr, src.astype(np.int64))
+        dg = kernels.device_graph(g)
+        for nodes in (np.arange(n), np.sort(rng.choice(n, n // 3, replace=False))):
+            for seed, layer in ((0, 1), (-3, 2)):
+                h = sample_neighbors(g, nodes, fanout, seed, layer)
+                d = sample_neighbors(dg, nodes, fanout, seed, layer)
+                assert np.array_equal(h.indptr, np.asarray(d.indptr_host))
+                assert np.array_equal(h.indices, d.indices.cpu().numpy().astype(np.int64))
