@@ -991,7 +991,7 @@ def infer_nodewise(m: ModelGraph, g, x_store, targets, batch_size, budget, stats
     def graph_for(layer):
         if sampled is not None and layer in sampled:
             if layer not in graphs:
-                graphs[layer] = DeviceGraph.from_host(sampled[layer], dg.device)
+                graphs[layer] = kernels.device_graph(sampled[layer], dg.device)
             return graphs[layer]
         return dg
 
@@ -1049,7 +1049,7 @@ def infer_nodewise(m: ModelGraph, g, x_store, targets, batch_size, budget, stats
                     op, [mats[p].index_select(0, rows_of(p, rows)) for p in op.inputs], params,
                     precision)
         prod = m.operators[m.output_id].inputs[0]
-        ck = torch.from_numpy(chunk).to(dg.device)
+        ck = torch.from_numpy(np.array(chunk, dtype=np.int64)).to(dg.device)
         out[start:start + len(chunk)] = mats[prod].index_select(0, rows_of(prod, ck))
         stats._add_batch(0, len(chunk), fp)
         for lay, cnt in sorted(agg_counts.items()):
@@ -1284,8 +1284,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
                      initial_thresholds=(thresholds.n_t, thresholds.n_i)
                      if executor == "layerwise" else None)
     started = time.perf_counter()
-    tsets = annotate(g_i if mode != "sampling" else g_i.to_host(), internal, m.depth, mode,
-                     fanout, seed)
+    tsets = annotate(g_i, internal, m.depth, mode, fanout, seed)   # device draws in sampling mode
     schedule = None
     if executor == "layerwise":
         schedule = split(m)
