@@ -112,6 +112,14 @@ def _ret(t, host):
     return t.cpu().numpy() if host else t
 
 
+def narrow_ids_into(out32, idx64, limit, bad):
+    """int64 -> int32 into `out32` on the current stream; bad (device int64[1])
+    receives the count of ids outside [0, limit) -- no host sync."""
+    _lib.call("glint_narrow_ids", idx64.shape[0], ptr(idx64), ptr(out32), int(limit), ptr(bad),
+              stream_handle())
+    return out32
+
+
 def narrow_ids(idx64, limit):
     """int64 -> int32 device ids, raising if any id is outside [0, limit)."""
     torch = _torch()

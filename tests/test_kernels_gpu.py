@@ -421,3 +421,44 @@ def test_device_sampling_matches_reference(golden, cuda):
                 d = sample_neighbors(dg, nodes, fanout, seed, layer)
                 assert np.array_equal(h.indptr, np.asarray(d.indptr_host))
                 assert np.array_equal(h.indices, d.indices.cpu().numpy().astype(np.int64))
+
+
+def test_streaming_graph_loader(tmp_path, cuda):
+    """load_graph_device (mmap + chunked pinned upload + device narrowing) gives
+    load_graph's arrays, and rejects the reference's malformed-file cases."""
+    import struct
+
+    from paper_2211_15082_b200.errors import FormatError
+    from paper_2211_15082_b200.storage import (CscGraph, load_graph, load_graph_device,
+                                               save_graph)
+
+    rng = np.random.default_rng(2)
+    n, e = 5000, 80000
+    dst = np.sort(rng.integers(0, n, size=e))
+    indptr = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+    g = CscGraph(n, e, indptr, rng.integers(0, n, size=e).astype(np.int64))
+    p = tmp_path / "g.dgig"
+    save_graph(g, p)
+    ref = load_graph(p)
+    for chunk in (1 << 25, 7777):
+        dg = load_graph_device(p, chunk_edges=chunk)
+        assert np.array_equal(np.asarray(dg.indptr_host), ref.indptr)
+        assert np.array_equal(dg.indptr.cpu().numpy(), ref.indptr)
+        assert np.array_equal(dg.indices.cpu().numpy().astype(np.int64), ref.indices)
+    empty = tmp_path / "e.dgig"
+    save_graph(CscGraph(3, 0, np.zeros(4, np.int64), np.zeros(0, np.int64)), empty)
+    assert load_graph_device(empty).num_edges == 0
+    raw = p.read_bytes()
+    cases = {
+        "magic": b"XXXX" + raw[4:],
+        "trunc": raw[:-8],
+        "trail": raw + b"\0",
+        "range": raw[:-8] + struct.pack("<Q", n),
+        "mono": raw[:struct.calcsize("<4sIQQ") + 8] + struct.pack("<Q", 10 ** 9)
+        + raw[struct.calcsize("<4sIQQ") + 16:],
+    }
+    for name, data in cases.items():
+        q = tmp_path / f"{name}.dgig"
+        q.write_bytes(data)
+        with pytest.raises(FormatError):
+            load_graph_device(q, chunk_edges=10000)
