@@ -175,6 +175,23 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim,
                             const float* s_src, const float* s_dst, float slope,
                             float* out, int64_t ld_out, const int32_t* schedule,
                             int64_t n_hub, int32_t act, glint_stream_t stream);
+/* The same result in two phases for the regular rows: an edge-softmax pass
+ * (SDDMM) writes every edge's H weights to the workspace, then a weighted
+ * SpMM streams them beside the Z rows (the K1 ring kernels) -- same weights,
+ * same accumulation order, same bytes.  Every regular row's edges must lie in
+ * [edge_base, edge_base + edge_span) of indptr; workspace from
+ * glint_gat_aggregate_workspace_bytes (NULL workspace = one-phase kernel). */
+size_t glint_gat_aggregate_workspace_bytes(int64_t n_rows, int64_t edge_span, int32_t heads);
+int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim,
+                               int32_t head_pitch, const int64_t* indptr,
+                               const int32_t* indices, const int64_t* row_ids,
+                               int64_t row_base, const int64_t* self_rows,
+                               const int32_t* col_map, const float* Z, int64_t ldz,
+                               const float* s_src, const float* s_dst, float slope,
+                               float* out, int64_t ld_out, const int32_t* schedule,
+                               int64_t n_hub, int32_t act, int64_t edge_base,
+                               int64_t edge_span, void* workspace, size_t workspace_bytes,
+                               glint_stream_t stream);
 
 /* --------------------------------------------------- K5 per-row operators
  * Replaces kernels.py:206-231 elementwise.  inputs / ld_inputs / input_rows

@@ -53,6 +53,10 @@ SIGNATURES = {
     "glint_gat_aggregate_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _P, _P, _I64, _P,
                                                _P, _P, _I64, _P, _P, _F32, _P, _I64, _P, _I64,
                                                _I32, _P]),
+    "glint_gat_aggregate_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
+    "glint_gat_aggregate_ws_f32": (ctypes.c_int, [_I64, _I32, _I32, _I32, _P, _P, _P, _I64, _P,
+                                                  _P, _P, _I64, _P, _P, _F32, _P, _I64, _P, _I64,
+                                                  _I32, _I64, _I64, _P, _SZ, _P]),
     "glint_elementwise_f32": (ctypes.c_int, [_I32, _I64, _I32, _I32, _P, _P, _P, _P, _I64, _P]),
     "glint_copy_rows_f32": (ctypes.c_int, [_I64, _I32, _P, _I64, _P, _P, _I64, _P, _P]),
     "glint_idset_workspace_bytes": (_SZ, [_I64]),
@@ -111,6 +115,7 @@ def last_error() -> str:
 KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
                     "glint_degree_prefix": 3, "glint_hub_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
                     "glint_rcmk_sorted_host": 0, "glint_sample_neighbors": 4,
+                    "glint_gat_aggregate_ws_f32": 2,
                     "glint_device_info": 0, "glint_set_tuning": 0, "glint_debug_counters": 0}
 LAUNCHES = [0]
 

@@ -885,6 +885,11 @@ struct GatArgs {
   float* __restrict__ out;
   int64_t ld_out;
   int act;
+  // two-phase path (glint_gat_aggregate_ws_f32): per-edge softmax weights
+  // W[(edge - w_base) * heads + h] and per-row self weights wself[r * heads + h]
+  float* __restrict__ w;
+  float* __restrict__ wself;
+  int64_t w_base;
 };
 
 __device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
@@ -1243,6 +1248,188 @@ __global__ void __launch_bounds__(kThreads, MINB) gat_async_kernel(GatArgs a) {
   gat_row_async<H, LPR, VPL, R>(a, r, lane_g, gmask, gring + threadIdx.x, sbase);
 }
 
+// ------------------------------------------------ two-phase GAT (SDDMM + SpMM) --
+//
+// Phase A, gat_softmax_kernel (edge softmax / SDDMM): LPR lanes per regular
+// row compute the per-head peak over self + edges, then every edge's H
+// weights w = exp(LeakyReLU(s_src[u] + s_dst[v]) - peak) -- lanes over edges,
+// stores coalesced along the row's edge range -- and the self weights.
+// Phase B, gat_spmm_async (weighted SpMM): the K1 ring machinery with each
+// lane also streaming its head's weight (4 bytes per edge, contiguous per
+// row); den += w, num += w z in stored edge order, self last.  Weights and
+// accumulation order are those of gat_row_regular, so the bytes match.
+template <int H, int LPR>
+__global__ void __launch_bounds__(kThreads) gat_softmax_kernel(GatArgs a) {
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t idx = a.sc.n_hub + static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
+  if (idx >= a.sc.n_rows) return;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  float sdst[H], peak[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    sdst[h] = __ldg(a.s_dst + self * H + h);
+    peak[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope);
+  }
+  for (int64_t e = beg + lane_g; e < end; e += LPR) {
+    const int64_t u = a.ra.map(a.ra.indices[e]);
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      peak[h] = fmaxf(peak[h], leaky(__fadd_rn(__ldg(a.s_src + u * H + h), sdst[h]), a.slope));
+  }
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1)
+      peak[h] = fmaxf(peak[h], __shfl_xor_sync(gmask, peak[h], o, LPR));
+  }
+  for (int64_t e = beg + lane_g; e < end; e += LPR) {
+    const int64_t u = a.ra.map(a.ra.indices[e]);
+    float* wp = a.w + (e - a.w_base) * H;
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      wp[h] = expf(__fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + u * H + h), sdst[h]), a.slope), peak[h]));
+  }
+  if (lane_g == 0) {
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      a.wself[r * H + h] =
+          expf(__fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope), peak[h]));
+  }
+}
+
+template <int H, int LPR, int VPL, int R>
+__device__ __forceinline__ void gat_spmm_row_async(const GatArgs& a, int64_t r, int lane_g,
+                                                   unsigned gmask, float4* zring, float* /*unused*/) {
+  // Z rows through the per-lane cp.async ring (as K1); the weights of the
+  // consume cursor's LPR-edge chunk sit in registers (lane i holds edge i's H
+  // weights, the next chunk prefetched) and reach every lane by H shuffles.
+  const int64_t rid = a.ra.csr_row(r);
+  const int64_t beg = a.ra.indptr[rid];
+  const int64_t end = a.ra.indptr[rid + 1];
+  const int64_t self = a.ra.self_row(r, rid);
+  const int deg = static_cast<int>(end - beg);
+  bool ok[VPL];
+  int hk[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int zc = (lane_g + LPR * k) * 4;
+    ok[k] = zc < H * a.head_pitch;
+    hk[k] = ok[k] ? zc / a.head_pitch : 0;
+  }
+  const uint32_t zr = smem_u32(zring);
+  const float* wrow = a.w + (beg - a.w_base) * H;
+  auto load_w = [&](int c0, float (&wv)[H]) {
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      wv[h] = (c0 + lane_g < deg) ? __ldg(wrow + static_cast<int64_t>(c0 + lane_g) * H + h) : 0.0f;
+  };
+  float wcur[H], wnxt[H];
+  load_w(0, wcur);
+  load_w(LPR, wnxt);
+  int ie = 0, cb = 0;
+  int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
+  int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
+  auto issue = [&](int slot) {
+    if (ie - cb == LPR) {
+      cb += LPR;
+      cur = nxt;
+      nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
+    }
+    const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
+    const float* zsrc = a.Z + u * a.ldz + lane_g * 4;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+      if (ok[k])
+        cp_async16(zr + static_cast<uint32_t>((slot * VPL + k) * kThreads) * 16u, zsrc + LPR * 4 * k);
+    ++ie;
+  };
+  float num[VPL][4], den[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    den[k] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) num[k][c] = 0.0f;
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    if (ie < deg) issue(t);
+    cp_async_commit();
+  }
+  int slot = 0, wc = 0;   // wc: consume cursor's position inside its weight chunk
+  for (int j = 0; j < deg; ++j) {
+    if (wc == LPR) {
+      wc = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) wcur[h] = wnxt[h];
+      load_w(j + LPR, wnxt);
+    }
+    float we[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) we[h] = __shfl_sync(gmask, wcur[h], wc, LPR);
+    ++wc;
+    cp_async_wait<R - 1>();
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (ok[k]) {
+        float w = we[0];
+#pragma unroll
+        for (int h = 1; h < H; ++h)
+          if (h == hk[k]) w = we[h];
+        const float4 v = zring[(slot * VPL + k) * kThreads];
+        den[k] = __fadd_rn(den[k], w);
+        num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v.x));
+        num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v.y));
+        num[k][2] = __fadd_rn(num[k][2], __fmul_rn(w, v.z));
+        num[k][3] = __fadd_rn(num[k][3], __fmul_rn(w, v.w));
+      }
+    }
+    if (ie < deg) issue(slot);
+    cp_async_commit();
+    slot = (slot + 1 == R) ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    if (!ok[k]) continue;
+    const int zc = (lane_g + LPR * k) * 4;
+    const int hh = hk[k];
+    const int jc = zc - hh * a.head_pitch;
+    const float4 zs = ldg_f4(a.Z + self * a.ldz + zc);
+    const float ws = a.wself[r * H + hh];
+    const float d = __fadd_rn(den[k], ws);
+    const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
+    float* dst = a.out + r * a.ld_out + hh * a.head_dim + jc;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (jc + c < a.head_dim)
+        dst[c] = gat_epilogue(a, __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d));
+  }
+}
+
+template <int H, int LPR, int VPL, int R, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) gat_spmm_async_kernel(GatArgs a) {
+  extern __shared__ __align__(16) float4 gring2[];
+  constexpr int G = 32 / LPR;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = lane / LPR;
+  const int lane_g = lane % LPR;
+  const int64_t idx = a.sc.n_hub + static_cast<int64_t>(blockIdx.x) * (kWarps * G) + warp * G + group;
+  if (idx >= a.sc.n_rows) return;
+  const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
+  gat_spmm_row_async<H, LPR, VPL, R>(a, r, lane_g, gmask, gring2 + threadIdx.x, nullptr);
+}
+
 // Hub rows (first n_hub schedule entries): one CTA per (row, 256-column block).
 __global__ void __launch_bounds__(kThreads) gat_hub_kernel(GatArgs a) {
   __shared__ int64_t s_off[kGatHubChunk];
@@ -1486,11 +1673,62 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
   return rc;
 }
 
+// Two-phase GAT launch: hub rows on the side stream (one-phase ring kernel),
+// regular rows as edge softmax then weighted SpMM on the caller's stream.
+template <int H, int LPR_A, int LPR, int VPL, int R, int MINB>
+int launch_gat2(const GatArgs& a, cudaStream_t s) {
+  SideStream* ss = nullptr;
+  if (a.sc.hub_ctas > 0) {
+    int rc = side_stream(&ss);
+    if (rc) return rc;
+    GLINT_CUDA(cudaEventRecord(ss->fork, s));
+    GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
+    rc = launch_gat_hub_ring(a, ss->stream);
+    if (rc) return rc;
+    GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
+  }
+  const int64_t regular = a.sc.n_rows - a.sc.n_hub;
+  if (regular > 0) {
+    const int64_t ga = ceil_div(regular, kWarps * (32 / LPR_A));
+    gat_softmax_kernel<H, LPR_A><<<static_cast<unsigned>(ga), kThreads, 0, s>>>(a);
+    int rc = launch_status("gat_softmax");
+    if (rc) return rc;
+    constexpr int smem = R * VPL * kThreads * 16;
+    static bool configured = false;
+    if (!configured) {
+      GLINT_CUDA(cudaFuncSetAttribute(gat_spmm_async_kernel<H, LPR, VPL, R, MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured = true;
+    }
+    const int64_t gb = ceil_div(regular, kWarps * (32 / LPR));
+    gat_spmm_async_kernel<H, LPR, VPL, R, MINB><<<static_cast<unsigned>(gb), kThreads, smem, s>>>(a);
+  }
+  const int rc = launch_status("gat_spmm");
+  if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+  return rc;
+}
+
 // chunks = 128-bit chunks per padded Z row.  Variants (GLINT_TUNE_GAT_VARIANT)
 // trade unroll depth against occupancy; 0 = default (best measured).
 template <int H>
 int dispatch_gat_h(const GatArgs& a, int chunks, cudaStream_t s) {
   const int v = tuning(GLINT_TUNE_GAT_VARIANT);
+  if (a.w != nullptr) {   // two-phase path (workspace given); variants 1-3 via the knob
+    if (chunks <= 16) return launch_gat2<H, 16, 16, 1, 8, 4>(a, s);
+    if (chunks <= 32) return launch_gat2<H, 16, 32, 1, 8, 4>(a, s);
+    if (chunks <= 48) {
+      if (v == 1) return launch_gat2<H, 16, 16, 3, 4, 3>(a, s);
+      if (v == 2) return launch_gat2<H, 16, 32, 2, 6, 3>(a, s);
+      if (v == 3) return launch_gat2<H, 8, 32, 2, 4, 4>(a, s);
+      return launch_gat2<H, 16, 32, 2, 4, 4>(a, s);
+    }
+    if (chunks <= 64) {
+      if (v == 1) return launch_gat2<H, 16, 32, 2, 3, 5>(a, s);
+      if (v == 2) return launch_gat2<H, 16, 32, 2, 6, 3>(a, s);
+      if (v == 3) return launch_gat2<H, 8, 32, 2, 4, 4>(a, s);
+      return launch_gat2<H, 16, 32, 2, 4, 4>(a, s);
+    }
+  }
   if (chunks <= 8) return launch_gat<H, 8, 1, 4, 6>(a, s);
   if (chunks <= 16) return launch_gat<H, 16, 1, 4, 6>(a, s);
   if (chunks <= 32) {
@@ -1604,12 +1842,30 @@ int glint_degree_schedule(int64_t n_rows, const int64_t* indptr, const int64_t* 
   return launch_status("degree_schedule");
 }
 
+size_t glint_gat_aggregate_workspace_bytes(int64_t n_rows, int64_t edge_span, int32_t heads) {
+  if (n_rows < 0 || edge_span < 0 || heads < 1) return 0;
+  const size_t w = (static_cast<size_t>(edge_span) * heads * 4 + 255) & ~static_cast<size_t>(255);
+  return w + static_cast<size_t>(n_rows) * heads * 4;
+}
+
 int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int32_t head_pitch,
                             const int64_t* indptr, const int32_t* indices, const int64_t* row_ids,
                             int64_t row_base, const int64_t* self_rows, const int32_t* col_map,
                             const float* Z, int64_t ldz, const float* s_src, const float* s_dst,
                             float slope, float* out, int64_t ld_out, const int32_t* schedule,
                             int64_t n_hub, int32_t act, glint_stream_t stream) {
+  return glint_gat_aggregate_ws_f32(n_rows, heads, head_dim, head_pitch, indptr, indices, row_ids,
+                                    row_base, self_rows, col_map, Z, ldz, s_src, s_dst, slope, out,
+                                    ld_out, schedule, n_hub, act, 0, 0, nullptr, 0, stream);
+}
+
+int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int32_t head_pitch,
+                               const int64_t* indptr, const int32_t* indices, const int64_t* row_ids,
+                               int64_t row_base, const int64_t* self_rows, const int32_t* col_map,
+                               const float* Z, int64_t ldz, const float* s_src, const float* s_dst,
+                               float slope, float* out, int64_t ld_out, const int32_t* schedule,
+                               int64_t n_hub, int32_t act, int64_t edge_base, int64_t edge_span,
+                               void* workspace, size_t workspace_bytes, glint_stream_t stream) {
   GLINT_REQUIRE(n_rows >= 0, "gat_aggregate: n_rows must be >= 0");
   if (n_rows == 0) return GLINT_OK;
   GLINT_REQUIRE(heads >= 1 && heads <= kMaxHeads, "gat_aggregate: heads must be in [1, %d]", kMaxHeads);
@@ -1641,6 +1897,17 @@ int glint_gat_aggregate_f32(int64_t n_rows, int32_t heads, int32_t head_dim, int
   a.sc.n_hub = n_hub;
   a.sc.hub_col_blocks = static_cast<int>(ceil_div(zw, kThreads));
   a.sc.hub_ctas = n_hub * a.sc.hub_col_blocks;
+  a.w = nullptr;
+  a.wself = nullptr;
+  a.w_base = edge_base;
+  if (workspace) {
+    GLINT_REQUIRE(edge_base >= 0 && edge_span >= 0, "gat_aggregate: bad edge range");
+    GLINT_REQUIRE(workspace_bytes >= glint_gat_aggregate_workspace_bytes(n_rows, edge_span, heads),
+                  "gat_aggregate: workspace too small");
+    const size_t wb = (static_cast<size_t>(edge_span) * heads * 4 + 255) & ~static_cast<size_t>(255);
+    a.w = static_cast<float*>(workspace);
+    a.wself = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + wb);
+  }
   const int chunks = zw / 4;
   cudaStream_t s = as_stream(stream);
   GLINT_REQUIRE(chunks <= 256, "gat_aggregate: heads*head_pitch must be <= 1024");

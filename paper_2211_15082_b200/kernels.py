@@ -473,9 +473,25 @@ def attn_project(h, w_pad, attn, heads, head_dim, precision=None):
     return Z, s_src, s_dst
 
 
+GAT_TWO_PHASE = True    # honoured when a caller passes edge_range (measured slower: profiles/r01_gat_sweep_two_phase.jsonl)
+
+
 def gat_aggregate(out, Z, s_src, s_dst, heads, head_dim, indptr, indices, n_rows, row_ids=None,
                   row_base=0, self_rows=None, col_map=None, schedule=None, n_hub=0,
-                  act=0):
+                  act=0, edge_range=None):
+    """K4.  edge_range=(base, span) covering every row's edges of indptr selects
+    the two-phase path (glint_gat_aggregate_ws_f32, same bytes)."""
+    if edge_range is not None and GAT_TWO_PHASE and int(n_rows) > 0:
+        base, span = (int(v) for v in edge_range)
+        torch = _torch()
+        wsb = _lib.query("glint_gat_aggregate_workspace_bytes", int(n_rows), span, heads)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=Z.device)
+        _lib.call("glint_gat_aggregate_ws_f32", int(n_rows), heads, head_dim,
+                  head_pitch(head_dim), ptr(indptr), ptr(indices), ptr(row_ids), int(row_base),
+                  ptr(self_rows), ptr(col_map), ptr(Z), ld(Z), ptr(s_src), ptr(s_dst),
+                  float(LEAKY_SLOPE), ptr(out), ld(out), ptr(schedule), int(n_hub), int(act),
+                  base, span, ptr(ws), wsb, stream_handle())
+        return out
     _lib.call("glint_gat_aggregate_f32", int(n_rows), heads, head_dim, head_pitch(head_dim),
               ptr(indptr), ptr(indices), ptr(row_ids), int(row_base), ptr(self_rows),
               ptr(col_map), ptr(Z), ld(Z), ptr(s_src), ptr(s_dst), float(LEAKY_SLOPE), ptr(out),

@@ -266,6 +266,21 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
             kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n,
                                   schedule=sched, n_hub=int(nh.item()))
             assert torch.equal(plain, outs[0]), v
+            # two-phase (edge softmax + weighted SpMM) path, whole and offset edge ranges
+            for rng_ in ((0, int(degs.sum())), (-5, int(degs.sum()) + 9)):
+                if rng_[0] < 0:
+                    continue
+                kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n,
+                                      schedule=sched, n_hub=int(nh.item()), edge_range=rng_)
+                assert torch.equal(plain, outs[0]), (v, rng_)
+            half = n // 2
+            e0 = int(degs[:half].sum())
+            part = torch.empty((n - half, heads * dh), device="cuda")
+            s2, nh2 = kernels.degree_schedule(indptr, None, half, n - half)
+            kernels.gat_aggregate(part, Z, s_src, s_dst, heads, dh, indptr, indices, n - half,
+                                  row_base=half, schedule=s2, n_hub=int(nh2.item()),
+                                  edge_range=(e0, int(degs.sum()) - e0))
+            assert torch.equal(part, outs[0][half:]), v
     finally:
         _lib.call("glint_set_tuning", 3, 0)
 

@@ -198,6 +198,18 @@ def sweep_gat(args, g, n):
             print(json.dumps({"kernel": "gat_aggregate", "heads": heads, "head_dim": dh,
                               "variant": variant, "ms": ms, "GBps": nb / ms / 1e6,
                               "identical_to_v0": same}), flush=True)
+        for variant in range(4):        # two-phase path (edge softmax + weighted SpMM)
+            _lib.call("glint_set_tuning", 3, variant)
+
+            def run2():
+                kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, g.indptr, g.indices, n,
+                                      schedule=sched, n_hub=n_hub, edge_range=(0, g.num_edges))
+
+            ms = timed(run2, args.reps)
+            print(json.dumps({"kernel": "gat_aggregate_two_phase", "heads": heads, "head_dim": dh,
+                              "variant": variant, "ms": ms,
+                              "GBps": agg_bytes(heads * hp, g.num_edges, n, heads=heads) / ms / 1e6,
+                              "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
         _lib.call("glint_set_tuning", 3, 0)
         del Z, out, ref
 
