@@ -41,6 +41,14 @@ int sm_count() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
       n = 148;
     cached[dev] = n;
+    // The library's stream-ordered scratch (cudaMallocAsync: the GEMM's W
+    // panel) comes from the device's default pool; keep freed blocks mapped
+    // instead of returning them at every synchronize (re-mapping costs ~ms).
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess && pool) {
+      uint64_t keep = 256ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
   }
   return cached[dev];
 }

@@ -198,6 +198,21 @@ def sweep_gat(args, g, n):
             print(json.dumps({"kernel": "gat_aggregate", "heads": heads, "head_dim": dh,
                               "variant": variant, "ms": ms, "GBps": nb / ms / 1e6,
                               "identical_to_v0": same}), flush=True)
+        for hub_knob in (1, 3):         # hub rows: register CTAs / TMA ring (default: LDGSTS ring)
+            _lib.call("glint_set_tuning", 3, 0)
+            _lib.call("glint_set_tuning", 2, hub_knob)
+            ms = timed(run, args.reps)
+            _lib.call("glint_set_tuning", 2, 0)
+            print(json.dumps({"kernel": "gat_aggregate_hub_path", "heads": heads, "head_dim": dh,
+                              "hub_knob": hub_knob, "ms": ms,
+                              "GBps": agg_bytes(heads * hp, g.num_edges, n, heads=heads) / ms / 1e6,
+                              "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+        _lib.call("glint_set_tuning", 3, 0)
+        ms = timed(lambda: kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, g.indptr,
+                                                 g.indices, n), args.reps)
+        print(json.dumps({"kernel": "gat_aggregate_no_hub_split", "heads": heads, "head_dim": dh,
+                          "ms": ms, "GBps": agg_bytes(heads * hp, g.num_edges, n, heads=heads) / ms / 1e6,
+                          "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
         for variant in range(4):        # two-phase path (edge softmax + weighted SpMM)
             _lib.call("glint_set_tuning", 3, variant)
 
