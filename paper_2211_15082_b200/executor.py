@@ -27,6 +27,7 @@ are computed on the host as in the reference and uploaded.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -394,7 +395,8 @@ class LayerwiseEngine:
         self.kernel_launches = 0
         self.probe = None               # optional KernelProbe (bench roofline timing)
         self.sink = None                # optional sink(store, row_lo, row_hi) for final rows
-        self.sink_chunks = 2            # each chunk is bounded by its slowest hub row
+        # output chunks streamed to the host sink (each is bounded by its slowest hub row)
+        self.sink_chunks = int(os.environ.get("GLINT_SINK_CHUNKS", "2"))
 
     # -- helpers ------------------------------------------------------------
 
