@@ -274,7 +274,7 @@ def config_block(args, n, und, desc, world):
     cfg = "cfg2" if args.model == "gcn3" else "cfg3"
     din, dh = 100, 256
     return {"workload": f"{cfg} {desc} full inference, OGBN-Products-shaped graph",
-            "nodes": n, "in_edges": 2 * und, "model": args.model, "mode": "full",
+            "nodes": n, "in_edges": 2 * und, "gnn": args.model, "mode": "full",
             "order": "none", "budget": "device (free HBM after resident stores)",
             "l2": "inputs larger than L2 (features %.2f GB, hidden %.2f GB per layer)"
                   % (n * din * 4 / 1e9, n * dh * 4 / 1e9),
