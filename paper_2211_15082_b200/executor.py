@@ -395,6 +395,7 @@ class LayerwiseEngine:
         self.kernel_launches = 0
         self.probe = None               # optional KernelProbe (bench roofline timing)
         self.sink = None                # optional sink(store, row_lo, row_hi) for final rows
+        self.exchange = None            # RowExchange of a distributed run (set by run())
         # output chunks streamed to the host sink (each is bounded by its slowest hub row)
         self.sink_chunks = int(os.environ.get("GLINT_SINK_CHUNKS", "2"))
 
@@ -742,14 +743,19 @@ class LayerwiseEngine:
                 h, cmap = conv_source(op.inputs[0])
                 d_in, d_out = int(h.shape[1]), m.out_dims[o]
                 if o not in gat_cache:
-                    z = torch.empty((h.shape[0], pitch_of(d_out)), dtype=torch.float32,
-                                    device=self.dev)[:, :d_out]
+                    zfull = torch.empty((h.shape[0], pitch_of(d_out)), dtype=torch.float32,
+                                        device=self.dev)
+                    z = zfull[:, :d_out]
+                    own = self._own_source_rows(h)
+                    lo, hi = own if own else (0, int(h.shape[0]))
                     if self.probe is not None:
                         self.probe.begin("linear")
-                    kernels.linear_into(z, h, self.params.w[o], None, _lib.ACT_NONE,
+                    kernels.linear_into(z[lo:hi], h[lo:hi], self.params.w[o], None, _lib.ACT_NONE,
                                         precision=self.precision)
                     if self.probe is not None:
-                        self.probe.end(2 * int(h.shape[0]) * d_in * d_out)
+                        self.probe.end(2 * (hi - lo) * d_in * d_out)
+                    if own:     # every rank sends its transformed rows (d_out wide, not d_in)
+                        self.exchange.exchange_tensor(zfull)
                     gat_cache[o] = z
                     self.kernel_launches += 1
                 act_op = fused.get(o)
@@ -798,13 +804,24 @@ class LayerwiseEngine:
                 W = op.params["weight"]
                 H, dh = int(W.shape[0]), int(W.shape[1])
                 if o not in gat_cache:
+                    own = self._own_source_rows(h)
+                    lo, hi = own if own else (0, int(h.shape[0]))
+                    n_src = int(h.shape[0])
+                    proj = (torch.empty((n_src, H * kernels.head_pitch(dh)), dtype=torch.float32,
+                                        device=self.dev),
+                            torch.empty((n_src, H), dtype=torch.float32, device=self.dev),
+                            torch.empty((n_src, H), dtype=torch.float32, device=self.dev))
                     if self.probe is not None:
                         self.probe.begin("linear")
-                    gat_cache[o] = kernels.attn_project(h, self.params.w_pad[o], self.params.attn[o],
-                                                        H, dh, precision=self.precision)
+                    kernels.attn_project(h[lo:hi], self.params.w_pad[o], self.params.attn[o], H, dh,
+                                         precision=self.precision,
+                                         out=tuple(t[lo:hi] for t in proj))
                     if self.probe is not None:
-                        self.probe.end(2 * int(h.shape[0]) * int(h.shape[1])
-                                       * H * kernels.head_pitch(dh))
+                        self.probe.end(2 * (hi - lo) * int(h.shape[1]) * H * kernels.head_pitch(dh))
+                    if own:     # exchange the projected rows and scores, not the source rows
+                        for t in proj:
+                            self.exchange.exchange_tensor(t)
+                    gat_cache[o] = proj
                     self.kernel_launches += 2
                 Z, s_src, s_dst = gat_cache[o]
                 act_op = fused.get(o)
@@ -869,7 +886,23 @@ class LayerwiseEngine:
                 if st is not None:
                     st.release()
 
+    def _own_source_rows(self, h):
+        """(lo, hi) when this rank should transform only its own rows of a full
+        source matrix and exchange the (narrower / per-head) result instead of
+        the source: distributed full mode with a whole-graph source."""
+        if self.exchange is None or self.row_range is None or h.shape[0] != self.g.num_nodes:
+            return None
+        return self.row_range
+
+    def transform_first(self, op_id) -> bool:
+        """Convs that transform every source row before aggregating (reassociated
+        ConvMean, ConvAttn): in distributed mode they exchange the transformed
+        rows, so their source store needs no exchange of its own."""
+        op = self.m.operators[op_id]
+        return op.kind == "ConvAttn" or (op.kind == "ConvMean" and self._reassociate(op_id))
+
     def run(self, exchange=None):
+        self.exchange = exchange
         if self.probe is not None:
             self.probe.mark("start")
         for blk in self.schedule.blocks:

@@ -457,14 +457,18 @@ def padded_head_weight(weight, device=None):
     return out.reshape(H * hp, K)
 
 
-def attn_project(h, w_pad, attn, heads, head_dim, precision=None):
-    """Z = h W_pad^T (head-padded) and the per-head scores s_src / s_dst."""
+def attn_project(h, w_pad, attn, heads, head_dim, precision=None, out=None):
+    """Z = h W_pad^T (head-padded) and the per-head scores s_src / s_dst
+    (into `out` = (Z, s_src, s_dst) row views when given)."""
     torch = _torch()
     hp = head_pitch(head_dim)
     M = h.shape[0]
-    Z = torch.empty((M, heads * hp), dtype=torch.float32, device=h.device)
-    s_src = torch.empty((M, heads), dtype=torch.float32, device=h.device)
-    s_dst = torch.empty((M, heads), dtype=torch.float32, device=h.device)
+    if out is not None:
+        Z, s_src, s_dst = out
+    else:
+        Z = torch.empty((M, heads * hp), dtype=torch.float32, device=h.device)
+        s_src = torch.empty((M, heads), dtype=torch.float32, device=h.device)
+        s_dst = torch.empty((M, heads), dtype=torch.float32, device=h.device)
     a = _f32(attn).contiguous()
     prec = PRECISION if precision is None else precision
     _lib.call("glint_gat_project_f32", M, heads, head_dim, hp, int(w_pad.shape[1]), ptr(h), ld(h),

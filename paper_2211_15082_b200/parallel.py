@@ -67,12 +67,21 @@ class RowExchange:
             w.wait()
 
     def __call__(self, engine, blk):
-        """Hook for LayerwiseEngine.run: exchange outputs later blocks read."""
+        """Hook for LayerwiseEngine.run: exchange outputs later blocks read.
+
+        A store whose every later reader transforms its source rows first
+        (reassociated ConvMean, ConvAttn) is skipped: those convs transform only
+        the rank's own rows and exchange the result, which is narrower (layer 3:
+        47 vs 256 columns) and spares every rank the other ranks' transforms."""
         from .splitter import TensorRef
 
         for o in blk.outputs:
             key = TensorRef(blk.block_id, o).key
             if key == engine.schedule.model_output.key:
                 continue
-            if engine.schedule.drop_after.get(key, blk.block_id) > blk.block_id:
-                self.exchange_tensor(engine.stores[key].data)
+            if engine.schedule.drop_after.get(key, blk.block_id) <= blk.block_id:
+                continue
+            readers = [c for c in engine.users.get(o, ()) if c not in blk.op_ids]
+            if readers and all(engine.transform_first(c) for c in readers):
+                continue
+            self.exchange_tensor(engine.stores[key].data)
