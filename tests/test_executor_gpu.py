@@ -197,3 +197,41 @@ def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
     lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 4
     assert all(x["bit_identical_all_ranks"] for x in lines), lines
+
+
+@pytest.mark.gpu
+def test_bench_json_contract():
+    """bench.py (small graph) prints one JSON line carrying every key the driver
+    reads, for both arms."""
+    import json
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    for extra in ([], ["--impl", "reference"]):
+        out = subprocess.run([sys.executable, str(root / "bench.py"), "--nodes", "20000",
+                              "--steps", "2", "--warmup", "3", "--cpu-sample", "256"] + extra,
+                             capture_output=True, text=True, timeout=600, cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+        assert len(lines) == 1
+        d = json.loads(lines[0])
+        for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                  "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                  "cpu_baseline", "e2e"):
+            assert k in d, k
+        assert d["value"] > 0 and "workload" in d["config"]
+        if extra:
+            assert d["impl"] == "reference" and d["e2e"]["h2d_bytes_per_step"] == 0
+        else:
+            for k in ("roofline", "gpu_launches", "clocks"):
+                assert k in d, k
+            r = d["roofline"]
+            for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+                assert k in r, k
+            assert d["gpu_launches"] > 0
+            for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+                assert k in d["e2e"], k
+            for k in ("value", "unit", "cores", "kind", "sample"):
+                assert k in d["cpu_baseline"], k
