@@ -593,8 +593,11 @@ class LayerwiseEngine:
             out_space = _RowSpace(targets_dev, ids.rank_map())
         for o in blk.outputs:
             key = TensorRef(blk.block_id, o).key
+            # full mode writes every row (own rows by the kernels, the others by
+            # the exchange), so the store needs no memset
             self.stores[key] = DeviceStore(len(targets_np), m.out_dims[o], self.dev,
-                                           rows=out_space.ids, rank_map=out_space.rank_map)
+                                           rows=out_space.ids, rank_map=out_space.rank_map,
+                                           zero_fill=not full)
             self.spaces[key] = out_space
 
         if blk.has_conv:
