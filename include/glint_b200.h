@@ -300,6 +300,23 @@ int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices,
  * reference's tie rules (reorder.py:55-123). perm_out[new] = old. */
 int glint_rcmk_host(int64_t num_nodes, const int64_t* indptr,
                     const int64_t* indices, int64_t* perm_out);
+/* Asynchronous CSR upload with host narrowing (upload.cu): a native thread
+ * narrows the int64 ids of edge chunk k = [chunk_edges[k], chunk_edges[k+1])
+ * on `threads` CPU threads into stage_pinned (caller's pinned int32 buffer),
+ * queues the H2D copy into dst_dev on copy_stream and records chunk k's event.
+ * glint_upload_wait blocks until chunk k is queued, then makes `stream` wait
+ * for it; glint_upload_query returns 1 once it has landed; glint_upload_finish
+ * joins the thread and frees the handle. */
+int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage_pinned,
+                       const int64_t* chunk_edges, int32_t n_chunks, int32_t threads,
+                       glint_stream_t copy_stream, void** handle_out);
+int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream);
+int glint_upload_query(void* handle, int32_t chunk);
+int glint_upload_finish(void* handle);
+/* Host int64 -> int32 narrowing on `threads` CPU threads (host pointers);
+ * returns the number of ids outside int32 (the e2e upload narrows CSR chunks
+ * on the host so they cross PCIe at half the bytes). */
+int64_t glint_narrow_ids_host(const int64_t* src, int32_t* dst, int64_t n, int32_t threads);
 /* The same order from a symmetrised adjacency whose rows are already
  * deduplicated, free of self loops and ordered by (degree, id) -- built on the
  * device by reorder._sorted_adjacency_device -- so the host pass is linear

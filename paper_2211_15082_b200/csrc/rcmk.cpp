@@ -178,3 +178,36 @@ extern "C" int glint_rcmk_sorted_host(int64_t n, const int64_t* ptr, const int32
   for (int64_t i = 0; i < n; ++i) perm_out[i] = seq[n - 1 - i];
   return GLINT_OK;
 }
+
+// Host int64 -> int32 id narrowing on `threads` threads (the e2e upload path
+// narrows CSR chunks on the CPU while the features cross PCIe, so the CSR
+// crosses as int32 -- half the bytes).  Ids must already be validated
+// (CscGraph checks [0, N) on construction); returns the count of ids that do
+// not fit int32 as a guard.
+#include <thread>
+
+extern "C" int64_t glint_narrow_ids_host(const int64_t* src, int32_t* dst, int64_t n,
+                                         int32_t threads) {
+  if (n <= 0) return 0;
+  if (!src || !dst) return -1;
+  int t = threads < 1 ? 1 : (threads > 64 ? 64 : threads);
+  if (n < (1 << 16)) t = 1;
+  std::vector<int64_t> bad(t, 0);
+  auto work = [&](int k) {
+    const int64_t lo = n * k / t, hi = n * (k + 1) / t;
+    int64_t b = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const int64_t v = src[i];
+      b += (v < INT32_MIN || v > INT32_MAX);
+      dst[i] = static_cast<int32_t>(v);
+    }
+    bad[k] = b;
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  int64_t total = 0;
+  for (int64_t b : bad) total += b;
+  return total;
+}

@@ -1,0 +1,157 @@
+// Asynchronous CSR upload with host-side int64 -> int32 narrowing.
+//
+// The reference hands the engine a host CscGraph with int64 ids
+// (storage.py:33-66); the device keeps int32 ids.  Narrowing on the host lets
+// the CSR cross PCIe at half the bytes (the e2e path's H2D is its floor), but
+// it must not hold the Python thread that launches layer-1 batches: a native
+// thread narrows row chunk k on `threads` CPU threads into the caller's pinned
+// staging buffer, queues its cudaMemcpyAsync on the copy stream and records
+// chunk k's event; consumers wait for "queued" on the host (condition
+// variable, no GIL held -- ctypes releases it) and then for the event on
+// their stream.
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace glint {
+namespace {
+
+struct Upload {
+  std::thread worker;
+  std::vector<cudaEvent_t> events;
+  std::vector<int64_t> bounds;   // K+1 edge offsets
+  std::vector<int> queued;       // guarded by mu
+  std::mutex mu;
+  std::condition_variable cv;
+  int error = 0;
+  int device = 0;
+};
+
+void narrow_parallel(const int64_t* src, int32_t* dst, int64_t n, int threads, int64_t* bad) {
+  const int t = (n < (1 << 16)) ? 1 : std::max(1, std::min(threads, 64));
+  std::vector<int64_t> b(t, 0);
+  auto work = [&](int k) {
+    const int64_t lo = n * k / t, hi = n * (k + 1) / t;
+    int64_t c = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const int64_t v = src[i];
+      c += (v < INT32_MIN || v > INT32_MAX);
+      dst[i] = static_cast<int32_t>(v);
+    }
+    b[k] = c;
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int64_t c : b) *bad += c;
+}
+
+}  // namespace
+}  // namespace glint
+
+using namespace glint;
+
+extern "C" {
+
+int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage_pinned,
+                       const int64_t* chunk_edges, int32_t n_chunks, int32_t threads,
+                       glint_stream_t copy_stream, void** handle_out) {
+  GLINT_REQUIRE(handle_out && n_chunks >= 0 && chunk_edges, "upload_start: bad argument");
+  GLINT_REQUIRE(n_chunks == 0 || (src_host && dst_dev && stage_pinned),
+                "upload_start: null buffer");
+  for (int k = 0; k < n_chunks; ++k)
+    GLINT_REQUIRE(chunk_edges[k] <= chunk_edges[k + 1] && chunk_edges[k] >= 0,
+                  "upload_start: chunk bounds must be non-decreasing");
+  auto* u = new Upload();
+  GLINT_CUDA(cudaGetDevice(&u->device));
+  u->bounds.assign(chunk_edges, chunk_edges + n_chunks + 1);
+  u->queued.assign(n_chunks, 0);
+  u->events.resize(n_chunks);
+  for (int k = 0; k < n_chunks; ++k)
+    GLINT_CUDA(cudaEventCreateWithFlags(&u->events[k], cudaEventDisableTiming));
+  cudaStream_t s = as_stream(copy_stream);
+  u->worker = std::thread([u, src_host, dst_dev, stage_pinned, threads, s]() {
+    cudaSetDevice(u->device);
+    for (size_t k = 0; k + 1 < u->bounds.size(); ++k) {
+      const int64_t e0 = u->bounds[k], e1 = u->bounds[k + 1];
+      int err = 0;
+      if (e1 > e0) {
+        int64_t bad = 0;
+        narrow_parallel(src_host + e0, stage_pinned + e0, e1 - e0, threads, &bad);
+        if (bad) err = GLINT_EINVAL;
+        else if (cudaMemcpyAsync(dst_dev + e0, stage_pinned + e0, (e1 - e0) * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, s) != cudaSuccess)
+          err = GLINT_ECUDA;
+      }
+      if (!err && cudaEventRecord(u->events[k], s) != cudaSuccess) err = GLINT_ECUDA;
+      {
+        std::lock_guard<std::mutex> lk(u->mu);
+        if (err) {
+          u->error = err;
+          for (auto& q : u->queued) q = 1;
+        } else {
+          u->queued[k] = 1;
+        }
+      }
+      u->cv.notify_all();
+      if (err) return;
+    }
+  });
+  *handle_out = u;
+  return GLINT_OK;
+}
+
+// Blocks until chunk k's copy is queued, then makes `stream` wait for it.
+int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream) {
+  auto* u = static_cast<Upload*>(handle);
+  GLINT_REQUIRE(u && chunk >= 0 && chunk < static_cast<int>(u->queued.size()),
+                "upload_wait: bad chunk");
+  {
+    std::unique_lock<std::mutex> lk(u->mu);
+    u->cv.wait(lk, [&] { return u->queued[chunk] != 0; });
+    if (u->error) {
+      set_error("upload: chunk failed (%s)", u->error == GLINT_EINVAL
+                ? "node ids do not fit int32" : "CUDA copy error");
+      return u->error;
+    }
+  }
+  GLINT_CUDA(cudaStreamWaitEvent(as_stream(stream), u->events[chunk], 0));
+  return GLINT_OK;
+}
+
+// 1 when chunk k has been queued and its copy has landed, 0 otherwise.
+int glint_upload_query(void* handle, int32_t chunk) {
+  auto* u = static_cast<Upload*>(handle);
+  GLINT_REQUIRE(u && chunk >= 0 && chunk < static_cast<int>(u->queued.size()),
+                "upload_query: bad chunk");
+  {
+    std::lock_guard<std::mutex> lk(u->mu);
+    if (u->error) {
+      set_error("upload: a chunk failed");
+      return u->error;
+    }
+    if (!u->queued[chunk]) return 0;
+  }
+  const cudaError_t e = cudaEventQuery(u->events[chunk]);
+  if (e == cudaErrorNotReady) return 0;
+  GLINT_CUDA(e);
+  return 1;
+}
+
+// Joins the worker and releases the events (call once, after the last wait).
+int glint_upload_finish(void* handle) {
+  auto* u = static_cast<Upload*>(handle);
+  if (!u) return GLINT_OK;
+  if (u->worker.joinable()) u->worker.join();
+  for (auto ev : u->events) cudaEventDestroy(ev);
+  const int err = u->error;
+  delete u;
+  return err ? GLINT_ECUDA : GLINT_OK;
+}
+
+}  // extern "C"

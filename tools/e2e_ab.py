@@ -1,0 +1,51 @@
+#!/usr/bin/env python
+"""e2e A/B: run_inference from pinned host buffers, timed like bench.py's e2e."""
+import json
+import pathlib
+import sys
+import time
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+
+
+def main():
+    import os
+
+    import torch
+
+    from paper_2211_15082_b200 import synth
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+    from paper_2211_15082_b200.storage import CscGraph
+
+    n, und = synth.PRODUCTS_NODES, synth.PRODUCTS_UNDIRECTED
+    m = synth.build_gcn(100, 256, 47, 3, seed=0)
+    g = synth.gen_products_like(n, und, seed=0, device="cuda")
+    xt = synth.gen_features_device(n, 100, seed=0)
+    ip = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    ip.copy_(torch.from_numpy(g.indptr_host))
+    ix = torch.empty(g.num_edges, dtype=torch.int64, pin_memory=True)
+    ix.copy_(g.indices.to(torch.int64).cpu())
+    xh = torch.empty((n, 100), dtype=torch.float32, pin_memory=True)
+    xh.copy_(xt.cpu())
+    hg = CscGraph(n, g.num_edges, ip.numpy(), ix.numpy())
+    del g, xt
+    budget = DeviceBudget(160 << 30)
+    run_inference(m, hg, xh, budget=budget, output="numpy")
+    torch.cuda.synchronize()
+    times = []
+    res = None
+    for _ in range(5):
+        res = None
+        t0 = time.perf_counter()
+        res = run_inference(m, hg, xh, budget=budget, output="numpy")
+        torch.cuda.synchronize()
+        times.append(1e3 * (time.perf_counter() - t0))
+    print(json.dumps({"host_narrow": os.environ.get("GLINT_HOST_NARROW", "1"),
+                      "chunks": os.environ.get("GLINT_UPLOAD_CHUNKS", "16"),
+                      "threads": os.environ.get("GLINT_NARROW_THREADS", "default"),
+                      "ms": [round(t, 1) for t in times]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
