@@ -1302,11 +1302,15 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             if probe is not None:
                 probe.mark("features uploaded (copy stream)", copy)
 
-        # int32 CSR (host-narrowed) lands fast enough that 4 row chunks overlap
-        # it with layer 1 without splitting the batches into hub-bound pieces
-        # (tools/e2e_ab.py: median 71.0 vs 74.1 ms with 16 device-narrowed chunks)
-        chunks = int(os.environ.get("GLINT_UPLOAD_CHUNKS", "4" if HOST_NARROW else "16"))
-        dg0 = DeviceGraph.upload_async(g, dev, copy, after_indptr=upload_features, chunks=chunks)
+        # int32 CSR (host-narrowed) lands fast enough that 5 geometric row chunks
+        # (1/16, 1/8, 1/4, 1/2, all of the edges) overlap it with layer 1's
+        # bootstrap batches without splitting them into hub-bound pieces
+        # (tools/e2e_ab.py: median 69.9 ms vs 71.0 uniform x4 vs 74.1 with 16
+        # device-narrowed int64 chunks; profiles/r01_e2e_upload_ab.jsonl)
+        chunks = int(os.environ.get("GLINT_UPLOAD_CHUNKS", "5" if HOST_NARROW else "16"))
+        geometric = os.environ.get("GLINT_UPLOAD_GEOMETRIC", "1" if HOST_NARROW else "0") == "1"
+        dg0 = DeviceGraph.upload_async(g, dev, copy, after_indptr=upload_features, chunks=chunks,
+                                       geometric=geometric)
         x0, x_ready = box["x"], box["ev"]
         if probe is not None:
             probe.mark("csr uploaded (copy stream)", copy)

@@ -42,7 +42,8 @@ def main():
         torch.cuda.synchronize()
         times.append(1e3 * (time.perf_counter() - t0))
     print(json.dumps({"host_narrow": os.environ.get("GLINT_HOST_NARROW", "1"),
-                      "chunks": os.environ.get("GLINT_UPLOAD_CHUNKS", "16"),
+                      "chunks": os.environ.get("GLINT_UPLOAD_CHUNKS", "default"),
+                      "geometric": os.environ.get("GLINT_UPLOAD_GEOMETRIC", "0"),
                       "threads": os.environ.get("GLINT_NARROW_THREADS", "default"),
                       "ms": [round(t, 1) for t in times]}), flush=True)
 
