@@ -644,6 +644,8 @@ class LayerwiseEngine:
                                 gat_cache)
                 if sink_store is not None:
                     self.sink(sink_store, c0, c1)
+                if full and self.exchange is not None and hasattr(self.exchange, "progress"):
+                    self.exchange.progress(self, blk, c1)   # overlap: send finished pieces
 
         # Speculation while the CSR is still uploading (full mode): a batch's rows
         # are launched before its planning count blocks the host (the count needs

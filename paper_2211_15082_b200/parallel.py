@@ -39,12 +39,72 @@ def edge_balanced_ranges(indptr_host, parts) -> np.ndarray:
 
 
 class RowExchange:
-    """After a block: broadcast each rank's slice of every store read later."""
+    """Broadcast each rank's slice of every store read later.
 
-    def __init__(self, cuts, rank, world, group=None):
+    Overlapped with the block: each rank range is cut into `chunks` pieces;
+    after every batch the engine reports how far its rows are done
+    (progress), and each fully computed piece is posted at once -- P root
+    broadcasts per piece, in the same (piece, root, store) order on every rank
+    -- on the collective stream, while the next batches compute.  The block
+    end posts whatever is left and waits."""
+
+    def __init__(self, cuts, rank, world, group=None, chunks=4):
         self.cuts = np.asarray(cuts, dtype=np.int64)
         self.rank, self.world, self.group = int(rank), int(world), group
+        self.chunks = max(1, int(chunks))
         self.bytes_sent = 0
+        self._blk = None
+        self._posted = 0
+        self._works = []
+
+    def _piece(self, k, c):
+        lo, hi = int(self.cuts[k]), int(self.cuts[k + 1])
+        return lo + (hi - lo) * c // self.chunks, lo + (hi - lo) * (c + 1) // self.chunks
+
+    def _keys(self, engine, blk):
+        from .splitter import TensorRef
+
+        keys = []
+        for o in blk.outputs:
+            key = TensorRef(blk.block_id, o).key
+            if key == engine.schedule.model_output.key:
+                continue
+            if engine.schedule.drop_after.get(key, blk.block_id) <= blk.block_id:
+                continue
+            readers = [c for c in engine.users.get(o, ()) if c not in blk.op_ids]
+            if readers and all(engine.transform_first(c) for c in readers):
+                continue
+            keys.append(key)
+        return keys
+
+    def _post(self, engine, keys, upto):
+        import torch.distributed as dist
+
+        while self._posted < upto:
+            c = self._posted
+            for k in range(self.world):
+                lo, hi = self._piece(k, c)
+                if hi <= lo:
+                    continue
+                for key in keys:
+                    part = engine.stores[key].data[lo:hi]
+                    if k == self.rank:
+                        self.bytes_sent += part.numel() * part.element_size()
+                    self._works.append(dist.broadcast(part, src=k, group=self.group,
+                                                      async_op=True))
+            self._posted += 1
+
+    def progress(self, engine, blk, done_hi):
+        """Rows [.., done_hi) of this rank's range are computed for `blk`."""
+        if self._blk is not blk:
+            self._blk, self._posted, self._works = blk, 0, []
+            self._keys_cache = self._keys(engine, blk)
+        if not self._keys_cache:
+            return
+        ready = 0
+        while ready < self.chunks and self._piece(self.rank, ready)[1] <= done_hi:
+            ready += 1
+        self._post(engine, self._keys_cache, ready)
 
     @property
     def row_range(self):
@@ -67,21 +127,17 @@ class RowExchange:
             w.wait()
 
     def __call__(self, engine, blk):
-        """Hook for LayerwiseEngine.run: exchange outputs later blocks read.
+        """Hook for LayerwiseEngine.run at the end of a block: post the pieces
+        not yet sent and wait for all of them.
 
         A store whose every later reader transforms its source rows first
         (reassociated ConvMean, ConvAttn) is skipped: those convs transform only
         the rank's own rows and exchange the result, which is narrower (layer 3:
         47 vs 256 columns) and spares every rank the other ranks' transforms."""
-        from .splitter import TensorRef
-
-        for o in blk.outputs:
-            key = TensorRef(blk.block_id, o).key
-            if key == engine.schedule.model_output.key:
-                continue
-            if engine.schedule.drop_after.get(key, blk.block_id) <= blk.block_id:
-                continue
-            readers = [c for c in engine.users.get(o, ()) if c not in blk.op_ids]
-            if readers and all(engine.transform_first(c) for c in readers):
-                continue
-            self.exchange_tensor(engine.stores[key].data)
+        if self._blk is not blk:
+            self._blk, self._posted, self._works = blk, 0, []
+            self._keys_cache = self._keys(engine, blk)
+        self._post(engine, self._keys_cache, self.chunks)
+        for w in self._works:
+            w.wait()
+        self._blk, self._posted, self._works = None, 0, []

@@ -73,3 +73,73 @@ def test_row_exchange_gloo(world):
     covered = sorted(r for _, _, _, r in results)
     assert covered[0][0] == 0 and covered[-1][1] == 37
     assert sum(b for _, _, b, _ in results) == 37 * 5 * 4
+
+
+class _Store:
+    def __init__(self, data):
+        self.data = data
+
+
+class _FakeSchedule:
+    def __init__(self):
+        from types import SimpleNamespace
+
+        self.model_output = SimpleNamespace(key="out")
+        self.drop_after = {"b1.h": 2}
+
+
+class _FakeEngine:
+    """Just what RowExchange reads: stores, schedule, users, transform_first."""
+
+    def __init__(self, data):
+        self.stores = {"b1.h": _Store(data)}
+        self.schedule = _FakeSchedule()
+        self.users = {"h": ["conv2"]}
+
+    def transform_first(self, op):
+        return False
+
+
+def _progress_worker(rank, world, port, n, dim, result_q):
+    from types import SimpleNamespace
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    indptr = np.arange(n + 1, dtype=np.int64) * 3
+    cuts = edge_balanced_ranges(indptr, world)
+    ex = RowExchange(cuts, rank, world, chunks=3)
+    data = torch.full((n, dim), -1.0)
+    eng = _FakeEngine(data)
+    blk = SimpleNamespace(block_id=1, outputs=["h"], op_ids=["conv1", "h"])
+    lo, hi = ex.row_range
+    # rows are computed in batches of uneven size; progress after each batch
+    step = max(1, (hi - lo) // 4 + rank)
+    for s in range(lo, hi, step):
+        e = min(hi, s + step)
+        data[s:e] = torch.arange(s, e, dtype=torch.float32)[:, None] * 10 + torch.arange(dim)
+        ex.progress(eng, blk, e)
+    ex(eng, blk)
+    want = torch.arange(n, dtype=torch.float32)[:, None] * 10 + torch.arange(dim)[None, :]
+    result_q.put((rank, bool(torch.equal(data, want)), ex.bytes_sent))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_exchange_overlapped_pieces_gloo(world):
+    """progress() posts finished pieces as batches complete (same order on every
+    rank even though the ranks' batches differ); the block end completes it."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_progress_worker, args=(r, world, port, 41, 3, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in results)
+    assert sum(b for _, _, b in results) == 41 * 3 * 4
