@@ -148,6 +148,7 @@ struct TcArgs {
   bool c_vec4;
   bool raw_hi;               // experiment knob GLINT_TUNE_GEMM_RAWHI (v1 kernel only)
   bool mma_only;             // diagnostics knob GLINT_TUNE_GEMM_PROF == 2 (v2 kernel)
+  bool skip_lo;              // diagnostics knob GLINT_TUNE_GEMM_PROF == 3: no lo pass (wrong results)
   // GAT projection epilogue (v2, SC = true): per-head scores of each output row
   const float* attn;         // [heads, 2 * head_dim]
   float* s_src;              // [M, heads]
@@ -521,15 +522,16 @@ constexpr int kThreads2 = 18 * 32;
 constexpr int kProducerThreads = kProducerWarps * 32;
 constexpr int kScMaxN = 512;               // widest Z row with the fused score epilogue
 
-template <int BN>
+template <int BN, int MH = 2>   // MH: 128-row M halves per tile (2: 256 x BN, 1: 128 x BN)
 struct Cfg2 {
-  static constexpr int A_BYTES = BM * BK * 4;  // one raw / lo slot (256 x 16 fp32)
+  static constexpr int TM = MH * HALF;           // tile rows
+  static constexpr int A_BYTES = TM * BK * 4;  // one raw / lo slot (TM x 16 fp32)
   static constexpr int W_BYTES = BN * BK * 4;  // one of W hi / lo
   static constexpr int RAW_OFF = 0;
   static constexpr int LO_OFF = RA * A_BYTES;
   static constexpr int W_OFF = LO_OFF + RL * A_BYTES;
   static constexpr int EPI_OFF = W_OFF + RW * 2 * W_BYTES;
-  static constexpr uint32_t ACC = 2 * BN;      // TMEM columns of one accumulator
+  static constexpr uint32_t ACC = MH * BN;     // TMEM columns of one accumulator
   static constexpr uint32_t TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128
                                     : 2 * ACC <= 256 ? 256 : 512;
   static constexpr int EPI_BYTES = kEpiWarps2 * 32 * EPI_LD * 4 + kEpiWarps2 * BN * 4;
@@ -661,9 +663,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <int BN, int ACT, bool SC = false>
+template <int BN, int ACT, bool SC = false, int MH = 2>
 __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const uint8_t* __restrict__ panel) {
-  using C = Cfg2<BN>;
+  using C = Cfg2<BN, MH>;
+  constexpr int PER = C::TM * 4 / kProducerThreads;   // 16-byte chunks per producer thread
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_empty[RA];
   __shared__ __align__(8) uint64_t lo_full[RL], lo_empty[RL];
@@ -713,14 +716,14 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
     // row q >> 2, k-chunk q & 3 -- it copies them (cp.async) and later turns
     // the same chunks into lo, so it only ever waits on its own copies.
     const int t = threadIdx.x;
-    int rows[4], chs[4];
-    uint32_t offs[4];
+    int rows[PER], chs[PER];
+    uint32_t offs[PER];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < PER; ++i) {
       const int q = t + kProducerThreads * i;
       rows[i] = q >> 2;
       chs[i] = q & 3;
-      offs[i] = (rows[i] >= HALF ? C::A_BYTES / 2 : 0) + tile_off(rows[i] & (HALF - 1), chs[i]);
+      offs[i] = (rows[i] / HALF) * (HALF * BK * 4) + tile_off(rows[i] & (HALF - 1), chs[i]);
     }
     const uint32_t raw_base = smem_addr(smem + C::RAW_OFF);
     auto issue = [&](int64_t idx) {
@@ -729,9 +732,9 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
       mbar_wait(&raw_empty[slot], (use & 1u) ^ 1u);
       const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
       const int kb = static_cast<int>(idx % nkb);
-      const int64_t m0 = (tile / a.n_tiles) * BM;
+      const int64_t m0 = (tile / a.n_tiles) * C::TM;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < PER; ++i) {
         const int64_t row = m0 + rows[i];
         const int k = kb * BK + 4 * chs[i];
         const bool ok = row < a.M && k < a.K;
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
       const uint8_t* raw = smem + C::RAW_OFF + rs * C::A_BYTES;
       uint8_t* lo = smem + C::LO_OFF + ls * C::A_BYTES;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < PER && !a.skip_lo; ++i) {   // a.skip_lo: diagnostics only
         const float4 v = *reinterpret_cast<const float4*>(raw + offs[i]);
         float4 l;
         l.x = __fsub_rn(v.x, __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
@@ -815,8 +818,8 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
             const uint64_t dwh = umma_desc(w_hi + step);
             const uint64_t dwl = umma_desc(w_lo + step);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t hoff = h * (C::A_BYTES / 2) + step;
+            for (int h = 0; h < MH; ++h) {
+              const uint32_t hoff = h * (HALF * BK * 4) + step;
               const uint32_t d = tmem + static_cast<uint32_t>(buf * C::ACC + h * BN);
               mma_tf32(d, umma_desc(a_lo + hoff), dwh, C::IDESC, (kb | j) != 0);
               mma_tf32(d, umma_desc(a_hi + hoff), dwl, C::IDESC, 1u);
@@ -834,9 +837,13 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   } else {
     // ------------------------------------------------------------- epilogue
     // 8 warps: warp w drains TMEM lane quarter (w % 4) (the tcgen05.ld access
-    // rule) of M half h = (w - kEpi2) / 4, i.e. 32 rows x BN columns.
+    // rule); pair index p = (w - kEpi2) / 4 picks the M half (MH = 2: 32 rows x
+    // BN columns) or the column half (MH = 1: 32 rows x BN/2 columns).
     const int q = warp & 3;
-    const int h = (warp - kEpi2) >> 2;
+    const int p = (warp - kEpi2) >> 2;
+    const int h = MH == 2 ? p : 0;
+    constexpr int CW_SPAN = MH == 2 ? BN : BN / 2;    // columns this warp drains
+    const int cbase = MH == 2 ? 0 : p * CW_SPAN;
     float* stage = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - kEpi2) * 32 * EPI_LD;
     float* bias_s = reinterpret_cast<float*>(smem + C::EPI_OFF) + kEpiWarps2 * 32 * EPI_LD +
                     (warp - kEpi2) * BN;
@@ -859,7 +866,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
       const int buf = static_cast<int>(it & 1);
       const uint32_t tuse = static_cast<uint32_t>(it >> 1);
-      const int64_t m0 = (tile / a.n_tiles) * BM;
+      const int64_t m0 = (tile / a.n_tiles) * C::TM;
       const int n0 = static_cast<int>(tile % a.n_tiles) * BN;
       if (has_bias && n0 != bias_n0) {
         __syncwarp();
@@ -872,15 +879,15 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
       {
         const int64_t row_base = m0 + h * HALF + q * 32;
         const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) +
-                               static_cast<uint32_t>(buf * C::ACC + h * BN);
+                               static_cast<uint32_t>(buf * C::ACC + h * BN + cbase);
         ScoreAcc st{-1, 0.0f, 0.0f};
 #pragma unroll 1
-        for (int c0 = 0; c0 + 32 <= BN; c0 += 32)
-          epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_s + c0, has_bias, row_base, n0 + c0,
-                                 lane, sc_tab, st);
-        if constexpr (BN % 32 == 16)
-          epi_chunk<16, ACT, SC>(a, tbase + (BN - 16), stage, bias_s + (BN - 16), has_bias,
-                                 row_base, n0 + BN - 16, lane, sc_tab, st);
+        for (int c0 = 0; c0 + 32 <= CW_SPAN; c0 += 32)
+          epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_s + cbase + c0, has_bias, row_base,
+                                 n0 + cbase + c0, lane, sc_tab, st);
+        if constexpr (CW_SPAN % 32 == 16)
+          epi_chunk<16, ACT, SC>(a, tbase + (CW_SPAN - 16), stage, bias_s + cbase + CW_SPAN - 16,
+                                 has_bias, row_base, n0 + cbase + CW_SPAN - 16, lane, sc_tab, st);
         if constexpr (SC) score_flush(a, st, row_base + lane);
       }
       fence_before();
@@ -896,18 +903,19 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   }
 }
 
-template <int BN, int ACT, bool SC = false>
+template <int BN, int ACT, bool SC = false, int MH = 2>
 int launch_v2(TcArgs a, cudaStream_t s) {
-  using C = Cfg2<BN>;
+  using C = Cfg2<BN, MH>;
   constexpr int smem = SC ? C::SMEM_SC : C::SMEM;
+  static_assert(smem <= 227 * 1024, "v2 GEMM shared memory over the per-CTA limit");
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT, SC>,
+    GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT, SC, MH>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
   a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
-  a.num_tiles = ceil_div(a.M, BM) * a.n_tiles;
+  a.num_tiles = ceil_div(a.M, C::TM) * a.n_tiles;
   a.nkb = static_cast<int>(ceil_div(a.K, BK));
   const size_t panel_bytes = static_cast<size_t>(a.n_tiles) * a.nkb * 2 * C::W_BYTES;
   void* panel = nullptr;
@@ -917,7 +925,7 @@ int launch_v2(TcArgs a, cudaStream_t s) {
   int rc = launch_status("linear_3xtf32_panel");
   if (rc == GLINT_OK) {
     const int64_t grid = std::min<int64_t>(a.num_tiles, sm_count());
-    gemm_v2_kernel<BN, ACT, SC><<<static_cast<unsigned>(grid), kThreads2, smem, s>>>(
+    gemm_v2_kernel<BN, ACT, SC, MH><<<static_cast<unsigned>(grid), kThreads2, smem, s>>>(
         a, static_cast<const uint8_t*>(panel));
     rc = launch_status("linear_3xtf32");
   }
@@ -925,15 +933,27 @@ int launch_v2(TcArgs a, cudaStream_t s) {
   return rc;
 }
 
-template <int BN>
+template <int BN, int MH = 2>
 int launch_v2_act(const TcArgs& a, int act, cudaStream_t s) {
-  if (act == GLINT_ACT_RELU) return launch_v2<BN, GLINT_ACT_RELU>(a, s);
-  if (act == GLINT_ACT_LEAKY_RELU) return launch_v2<BN, GLINT_ACT_LEAKY_RELU>(a, s);
-  return launch_v2<BN, GLINT_ACT_NONE>(a, s);
+  if (act == GLINT_ACT_RELU) return launch_v2<BN, GLINT_ACT_RELU, false, MH>(a, s);
+  if (act == GLINT_ACT_LEAKY_RELU) return launch_v2<BN, GLINT_ACT_LEAKY_RELU, false, MH>(a, s);
+  return launch_v2<BN, GLINT_ACT_NONE, false, MH>(a, s);
 }
 
-// BN = N split into ceil(N/128) tiles, rounded up to an instantiated width.
+// N in (128, 256]: 128-row tiles with ONE N = BN MMA per product (each A row
+// is loaded and split once for all columns; knob GLINT_TUNE_GEMM_WIDE = 2
+// forces the 256-row x N/2 tiles).  N <= 128: 256-row tiles, BN = N rounded
+// up to an instantiated width.
 int launch_v2_bn(const TcArgs& a, int act, cudaStream_t s) {
+  if (a.N > 128 && a.N <= 256 && tuning(GLINT_TUNE_GEMM_WIDE) != 2) {
+    if (a.N <= 192) return launch_v2_act<192, 1>(a, act, s);
+    return launch_v2_act<256, 1>(a, act, s);
+  }
+  if (a.N <= 128 && tuning(GLINT_TUNE_GEMM_WIDE) == 3) {   // experiment: 128-row tiles
+    if (a.N <= 48) return launch_v2_act<48, 1>(a, act, s);
+    if (a.N <= 64) return launch_v2_act<64, 1>(a, act, s);
+    return launch_v2_act<128, 1>(a, act, s);
+  }
   const int nt = static_cast<int>(ceil_div(a.N, 128));
   const int per = static_cast<int>(ceil_div(a.N, nt));
   if (per <= 32) return launch_v2_act<32>(a, act, s);
@@ -945,6 +965,10 @@ int launch_v2_bn(const TcArgs& a, int act, cudaStream_t s) {
 
 // GAT projection with fused scores: needs every head inside one n-tile.
 int launch_v2_scores(const TcArgs& a, cudaStream_t s) {
+  if (a.N > 128 && a.N <= 256 && tuning(GLINT_TUNE_GEMM_WIDE) != 2) {
+    if (a.N <= 192) return launch_v2<192, GLINT_ACT_NONE, true, 1>(a, s);
+    return launch_v2<256, GLINT_ACT_NONE, true, 1>(a, s);
+  }
   const int nt = static_cast<int>(ceil_div(a.N, 128));
   const int per = static_cast<int>(ceil_div(a.N, nt));
   auto fits = [&](int bn) { return ceil_div(a.N, bn) == 1 || bn % a.head_pitch == 0; };
@@ -1008,6 +1032,7 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
   a.c_vec4 = (ldc % 4 == 0) && aligned16(C);
   a.raw_hi = tuning(GLINT_TUNE_GEMM_RAWHI) != 0;
   a.mma_only = tuning(GLINT_TUNE_GEMM_PROF) == 2;
+  a.skip_lo = tuning(GLINT_TUNE_GEMM_PROF) == 3;
   a.prof = nullptr;
   if (tuning(GLINT_TUNE_GEMM_PROF) == 1) {
     void* p = nullptr;

@@ -250,11 +250,26 @@ def gemm_only(args, n):
                               "TFLOPs": 2 * n * K * N / ms / 1e9,
                               "GBps": (n * K * 4 + n * N * 4) / ms / 1e6}), flush=True)
         _lib.call("glint_set_tuning", 4, 0)
-        _lib.call("glint_set_tuning", 1, 2)     # v2 with MMA issue only (no operand traffic)
-        ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
-        _lib.call("glint_set_tuning", 1, 0)
-        print(json.dumps({"kernel": "linear_mma_only", "K": K, "N": N, "ms": ms,
-                          "TFLOPs": 2 * n * K * N / ms / 1e9}), flush=True)
+        if N <= 128:                    # 128-row tiles (experiment knob 7 = 3)
+            _lib.call("glint_set_tuning", 7, 3)
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
+            _lib.call("glint_set_tuning", 7, 0)
+            print(json.dumps({"kernel": "linear_128row_tiles", "K": K, "N": N, "ms": ms,
+                              "TFLOPs": 2 * n * K * N / ms / 1e9,
+                              "identical": bool(torch.equal(c, outs[0]))}), flush=True)
+        if 128 < N <= 256:              # 256-row x N/2 tiles instead of 128-row x N
+            _lib.call("glint_set_tuning", 7, 2)
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
+            _lib.call("glint_set_tuning", 7, 0)
+            print(json.dumps({"kernel": "linear_256row_tiles", "K": K, "N": N, "ms": ms,
+                              "TFLOPs": 2 * n * K * N / ms / 1e9,
+                              "identical": bool(torch.equal(c, outs[0]))}), flush=True)
+        for diag, name in ((2, "linear_mma_only"), (3, "linear_no_lo_pass")):
+            _lib.call("glint_set_tuning", 1, diag)   # diagnostics (wrong results)
+            ms = timed(lambda: kernels.linear_into(c, a, w, b, 1, precision=1), args.reps)
+            _lib.call("glint_set_tuning", 1, 0)
+            print(json.dumps({"kernel": name, "K": K, "N": N, "ms": ms,
+                              "TFLOPs": 2 * n * K * N / ms / 1e9}), flush=True)
         print(json.dumps({"kernel": "linear_v1_v2_identical", "K": K, "N": N,
                           "identical": bool(torch.equal(outs[0], outs[1]))}), flush=True)
 
