@@ -19,7 +19,9 @@ def main():
     from paper_2211_15082_b200.storage import CscGraph
 
     n, und = synth.PRODUCTS_NODES, synth.PRODUCTS_UNDIRECTED
-    m = synth.build_gcn(100, 256, 47, 3, seed=0)
+    model = sys.argv[1] if len(sys.argv) > 1 else "gcn3"
+    m = (synth.build_gcn(100, 256, 47, 3, seed=0) if model == "gcn3"
+         else synth.build_gat(100, 64, 47, 3, heads=4, seed=0))
     g = synth.gen_products_like(n, und, seed=0, device="cuda")
     xt = synth.gen_features_device(n, 100, seed=0)
     ip = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
@@ -41,7 +43,8 @@ def main():
         res = run_inference(m, hg, xh, budget=budget, output="numpy")
         torch.cuda.synchronize()
         times.append(1e3 * (time.perf_counter() - t0))
-    print(json.dumps({"host_narrow": os.environ.get("GLINT_HOST_NARROW", "1"),
+    print(json.dumps({"model": model, "sink_chunks": os.environ.get("GLINT_SINK_CHUNKS", "2"),
+                      "host_narrow": os.environ.get("GLINT_HOST_NARROW", "1"),
                       "chunks": os.environ.get("GLINT_UPLOAD_CHUNKS", "default"),
                       "geometric": os.environ.get("GLINT_UPLOAD_GEOMETRIC", "0"),
                       "threads": os.environ.get("GLINT_NARROW_THREADS", "default"),
