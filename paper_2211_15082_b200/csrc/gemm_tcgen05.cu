@@ -515,12 +515,22 @@ namespace v2 {
 constexpr int RA = 6;   // raw-A ring (cp.async, also the TF32 "hi" operand)
 constexpr int RL = 2;   // A "lo" ring (computed by the producers)
 constexpr int RW = 3;   // W panel ring (TMA bulk copies)
-constexpr int kWarpW = 9;                  // W-panel loader warp
-constexpr int kEpi2 = 10;                  // 8 epilogue warps 10..17: (lane quarter, M half)
 constexpr int kEpiWarps2 = 8;
-constexpr int kThreads2 = 18 * 32;
-constexpr int kProducerThreads = kProducerWarps * 32;
 constexpr int kScMaxN = 512;               // widest Z row with the fused score epilogue
+
+// Warp roles: PW producer warps, then the MMA warp, the W loader and 8
+// epilogue warps.  8 producer warps measured faster than 4 for both tile
+// shapes, although 18 warps cap the kernel at 96 registers (the fused GAT
+// score epilogue then spills a little; profiles/r01_gemm_sweep.jsonl).
+template <int MH>
+struct Roles {
+  static constexpr int PW = 8;
+  static constexpr int MMA = PW;
+  static constexpr int WL = PW + 1;
+  static constexpr int EPI = PW + 2;
+  static constexpr int THREADS = (PW + 2 + kEpiWarps2) * 32;
+  static constexpr int PT = PW * 32;
+};
 
 template <int BN, int MH = 2>   // MH: 128-row M halves per tile (2: 256 x BN, 1: 128 x BN)
 struct Cfg2 {
@@ -604,22 +614,33 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, uint32_t taddr, float
     v[i] = col < a.N ? epilogue_op<ACT>(v[i], bias_s + i, has_bias) : 0.0f;
   }
   if constexpr (SC) {
-    // sc_tab: [0, N) a_src per column, [kScMaxN, +N) a_dst, [2 kScMaxN, +N) head
+    // sc_tab: [0, N) a_src per column, [kScMaxN, +N) a_dst.  The columns of a
+    // head are contiguous, so the chunk splits into at most a few head runs:
+    // the head changes at warp-uniform positions (no per-element lookup or
+    // divergence); each head's dot products stay one sequential fmaf chain.
     const int64_t row = row_base + lane;
+    int h = min(col0 / a.head_pitch, a.heads - 1);
+    int next = (h + 1) * a.head_pitch;      // first column of the following head
+    if (h != st.h) {
+      score_flush(a, st, row);
+      st.h = h;
+      st.ps = 0.0f;
+      st.pd = 0.0f;
+    }
 #pragma unroll
     for (int i = 0; i < CW; ++i) {
       const int col = col0 + i;
-      if (col < a.N) {
-        const int h = __float_as_int(sc_tab[2 * kScMaxN + col]);
-        if (h != st.h) {
-          score_flush(a, st, row);
-          st.h = h;
-          st.ps = 0.0f;
-          st.pd = 0.0f;
-        }
-        st.ps = fmaf(v[i], sc_tab[col], st.ps);
-        st.pd = fmaf(v[i], sc_tab[kScMaxN + col], st.pd);
+      if (col >= a.N) break;
+      if (col == next && h + 1 < a.heads) {
+        score_flush(a, st, row);
+        ++h;
+        next += a.head_pitch;
+        st.h = h;
+        st.ps = 0.0f;
+        st.pd = 0.0f;
       }
+      st.ps = fmaf(v[i], sc_tab[col], st.ps);
+      st.pd = fmaf(v[i], sc_tab[kScMaxN + col], st.pd);
     }
   }
 #pragma unroll
@@ -664,9 +685,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int BN, int ACT, bool SC = false, int MH = 2>
-__global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const uint8_t* __restrict__ panel) {
+__global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a, const uint8_t* __restrict__ panel) {
   using C = Cfg2<BN, MH>;
-  constexpr int PER = C::TM * 4 / kProducerThreads;   // 16-byte chunks per producer thread
+  using Rl = Roles<MH>;
+  constexpr int PER = C::TM * 4 / Rl::PT;   // 16-byte chunks per producer thread
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_empty[RA];
   __shared__ __align__(8) uint64_t lo_full[RL], lo_empty[RL];
@@ -677,7 +699,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp == kMmaWarp) {
+  if (warp == Rl::MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  :
                  : "r"(smem_addr(&tmem_slot)), "r"(C::TCOLS));
@@ -686,7 +708,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   if (threadIdx.x == 0) {
     for (int i = 0; i < RA; ++i) mbar_init(&raw_empty[i], 1);           // tcgen05.commit
     for (int i = 0; i < RL; ++i) {
-      mbar_init(&lo_full[i], kProducerWarps);                           // one per producer warp
+      mbar_init(&lo_full[i], Rl::PW);                           // one per producer warp
       mbar_init(&lo_empty[i], 1);
     }
     for (int i = 0; i < RW; ++i) {
@@ -708,9 +730,9 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
                                ? (a.num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = my_tiles * nkb;
 
-  if (a.mma_only && (warp < kProducerWarps || warp == kWarpW)) {
+  if (a.mma_only && (warp < Rl::PW || warp == Rl::WL)) {
     // diagnostics: no operand traffic
-  } else if (warp < kProducerWarps) {
+  } else if (warp < Rl::PW) {
     // ---------------------------------------------------------- producers
     // Thread t owns 16-byte chunks q = t + 256 i (i < 4) of every k-step:
     // row q >> 2, k-chunk q & 3 -- it copies them (cp.async) and later turns
@@ -720,7 +742,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
     uint32_t offs[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      const int q = t + kProducerThreads * i;
+      const int q = t + Rl::PT * i;
       rows[i] = q >> 2;
       chs[i] = q & 3;
       offs[i] = (rows[i] / HALF) * (HALF * BK * 4) + tile_off(rows[i] & (HALF - 1), chs[i]);
@@ -773,7 +795,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-  } else if (warp == kWarpW) {
+  } else if (warp == Rl::WL) {
     // ------------------------------------------------- W panel loader (TMA)
     if (lane == 0) {
       for (int64_t idx = 0; idx < total; ++idx) {
@@ -789,7 +811,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
                  &w_full[s]);
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == Rl::MMA) {
     // ------------------------------------------------------------ MMA issue
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
@@ -837,21 +859,21 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   } else {
     // ------------------------------------------------------------- epilogue
     // 8 warps: warp w drains TMEM lane quarter (w % 4) (the tcgen05.ld access
-    // rule); pair index p = (w - kEpi2) / 4 picks the M half (MH = 2: 32 rows x
+    // rule); pair index p = (w - Rl::EPI) / 4 picks the M half (MH = 2: 32 rows x
     // BN columns) or the column half (MH = 1: 32 rows x BN/2 columns).
     const int q = warp & 3;
-    const int p = (warp - kEpi2) >> 2;
+    const int p = (warp - Rl::EPI) >> 2;
     const int h = MH == 2 ? p : 0;
     constexpr int CW_SPAN = MH == 2 ? BN : BN / 2;    // columns this warp drains
     const int cbase = MH == 2 ? 0 : p * CW_SPAN;
-    float* stage = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - kEpi2) * 32 * EPI_LD;
+    float* stage = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - Rl::EPI) * 32 * EPI_LD;
     float* bias_s = reinterpret_cast<float*>(smem + C::EPI_OFF) + kEpiWarps2 * 32 * EPI_LD +
-                    (warp - kEpi2) * BN;
+                    (warp - Rl::EPI) * BN;
     const bool has_bias = a.bias != nullptr;
     float* sc_tab = reinterpret_cast<float*>(smem + C::SC_OFF);
     if constexpr (SC) {
       // per-column a_src / a_dst / head tables, shared by the 8 epilogue warps
-      for (int c = threadIdx.x - kEpi2 * 32; c < a.N; c += kEpiWarps2 * 32) {
+      for (int c = threadIdx.x - Rl::EPI * 32; c < a.N; c += kEpiWarps2 * 32) {
         const int hh = c / a.head_pitch;
         const int j = c - hh * a.head_pitch;
         const bool live = hh < a.heads && j < a.head_dim;
@@ -897,7 +919,7 @@ __global__ void __launch_bounds__(kThreads2, 1) gemm_v2_kernel(TcArgs a, const u
   }
   fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == Rl::MMA) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" : : "r"(tmem), "r"(C::TCOLS));
   }
@@ -925,7 +947,7 @@ int launch_v2(TcArgs a, cudaStream_t s) {
   int rc = launch_status("linear_3xtf32_panel");
   if (rc == GLINT_OK) {
     const int64_t grid = std::min<int64_t>(a.num_tiles, sm_count());
-    gemm_v2_kernel<BN, ACT, SC, MH><<<static_cast<unsigned>(grid), kThreads2, smem, s>>>(
+    gemm_v2_kernel<BN, ACT, SC, MH><<<static_cast<unsigned>(grid), Roles<MH>::THREADS, smem, s>>>(
         a, static_cast<const uint8_t*>(panel));
     rc = launch_status("linear_3xtf32");
   }

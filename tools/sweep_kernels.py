@@ -47,12 +47,16 @@ def main():
     ap.add_argument("--gemm", default="100x256,256x256,256x47,256x192,100x192")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
+    args.what = set(args.what.split(","))
     n = args.nodes
     und = int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES))
     g = synth.gen_products_like(n, und, seed=0, device="cuda") \
         if ("spmm" in args.what or "gat" in args.what) else None
     if g is None:
-        gemm_only(args, n)
+        if "gatproj" in args.what:
+            sweep_gat_project(args, n)
+        if "gemm" in args.what:
+            gemm_only(args, n)
         return
     deg = g.in_degrees
     hub_pre = int(((deg + 1) >= kernels.HUB_MIN_DEGREE).sum())
@@ -227,6 +231,28 @@ def sweep_gat(args, g, n):
                               "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
         _lib.call("glint_set_tuning", 3, 0)
         del Z, out, ref
+
+
+def sweep_gat_project(args, n):
+    """GAT projection with the fused score epilogue vs the plain GEMM + scores kernel."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels
+
+    for K, H, dh in ((100, 4, 64), (256, 4, 64), (256, 4, 47)):
+        h = torch.randn((n, K), device="cuda")
+        w = torch.randn((H, dh, K), device="cuda") / K ** 0.5
+        att = torch.randn((H, 2 * dh), device="cuda")
+        wp = kernels.padded_head_weight(w)
+        fused = timed(lambda: kernels.attn_project(h, wp, att, H, dh, precision=1), args.reps)
+        Z, s1, s2 = kernels.attn_project(h, wp, att, H, dh, precision=1)
+        hp = kernels.head_pitch(dh)
+        Zp = torch.empty((n, H * hp), device="cuda")
+        plain = timed(lambda: kernels.linear_into(Zp, h, wp, None, 0, precision=1), args.reps)
+        print(json.dumps({"kernel": "gat_project", "K": K, "heads": H, "head_dim": dh,
+                          "ms_fused_scores": fused, "ms_gemm_only": plain,
+                          "Z_identical": bool(torch.equal(Z, Zp))}), flush=True)
+        del h, Z, Zp
 
 
 def gemm_only(args, n):
