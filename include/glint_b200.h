@@ -76,7 +76,8 @@ int glint_abi_version(void);
 #define GLINT_TUNE_GEMM_RAWHI 5   /* experiment: unmasked fp32 as the tf32 "hi" operand */
 #define GLINT_TUNE_HUB_CTAS_PER_SM 6 /* K1 register hub kernel: k > 0 caps it at k CTAs per SM */
 #define GLINT_TUNE_GEMM_WIDE 7    /* K2, N in (128, 256]: 0 = 128 x N tiles, 2 = 256 x N/2 tiles */
-#define GLINT_TUNE_COUNT 8
+#define GLINT_TUNE_HUB_AFTER 8     /* hub-row kernels: 0 concurrent (side stream), 1 after the regular rows */
+#define GLINT_TUNE_COUNT 12
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of

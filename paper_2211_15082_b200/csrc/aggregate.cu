@@ -692,6 +692,13 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
   // CTAs, 2/3/4 ring CTAs (LDGSTS 32-col / TMA 32-col / LDGSTS 64-col),
   // 5 one-warp cp.async units (per-warp request limit: ~116 ns per edge).
   const int knob = tuning(GLINT_TUNE_HUB_INLINE);
+  if (tuning(GLINT_TUNE_HUB_AFTER) == 1) {   // hub rows after the regular rows, same stream
+    int rc = dispatch_regular(a, vec4, s);
+    if (rc) return rc;
+    if (vec4 && (knob >= 2 || (knob == 0 && a.sc.n_rows < (1 << 19)))) return launch_hub(a, s);
+    mean_hub_reg_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, s>>>(a);
+    return launch_status("spmm_mean_hub");
+  }
   SideStream* ss = nullptr;
   int rc = side_stream(&ss);
   if (rc) return rc;
@@ -1449,20 +1456,20 @@ __global__ void __launch_bounds__(kThreads) gat_hub_kernel(GatArgs a) {
 // stored edge order: den += w, num += w*z, self last -- the same arithmetic
 // and order as gat_row_regular.
 constexpr int kGatWChunk = 2048;
-constexpr int kConsumers = kHubConsumerWarps * 32;
-
+template <int CW>   // consumer warps (columns per CTA / 32)
 __device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
 }
 
-__global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, int slots_per_group,
+template <int CW>
+__global__ void __launch_bounds__((CW + 1) * 32) gat_hub_ring_kernel(GatArgs a, int slots_per_group,
                                                                    int slice_floats,
                                                                    int col_blocks, bool bulk) {
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full_bar[kHubGroups];
   __shared__ __align__(8) uint64_t empty_bar[kHubGroups];
   __shared__ float s_sd[kMaxHeads], s_pk[kMaxHeads];
-  __shared__ float s_red[kHubConsumerWarps][kMaxHeads];
+  __shared__ float s_red[CW][kMaxHeads];
   const int H = a.heads;
   float* w_sm = ring + kHubGroups * slots_per_group * slice_floats;  // [kGatWChunk][H]
   const int cb = static_cast<int>(blockIdx.x % col_blocks);
@@ -1483,13 +1490,13 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
                    ::"r"(smem_u32(&full_bar[g])), "r"(bulk ? 1 : 32));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
-                   ::"r"(smem_u32(&empty_bar[g])), "r"(kHubConsumerWarps));
+                   ::"r"(smem_u32(&empty_bar[g])), "r"(CW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kHubConsumerWarps) {
+  if (warp == CW) {
     hub_produce(a.ra, beg, end, a.Z, a.ldz, c0, width, slots_per_group, slice_floats, ring,
                 full_bar, empty_bar, bulk);
     return;
@@ -1506,7 +1513,7 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
         pk[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sd[h]), a.slope);
       }
     }
-    for (int64_t e = beg + tid; e < end; e += kConsumers) {
+    for (int64_t e = beg + tid; e < end; e += (CW * 32)) {
       const int64_t u = a.ra.map(a.ra.indices[e]);
 #pragma unroll
       for (int h = 0; h < kMaxHeads; ++h)
@@ -1521,13 +1528,13 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
         if (tid == 0) s_sd[h] = sd[h];
       }
     }
-    consumer_sync();
+    consumer_sync<CW>();
     if (tid < H) {
       float m = s_red[0][tid];
-      for (int w = 1; w < kHubConsumerWarps; ++w) m = fmaxf(m, s_red[w][tid]);
+      for (int w = 1; w < CW; ++w) m = fmaxf(m, s_red[w][tid]);
       s_pk[tid] = m;
     }
-    consumer_sync();
+    consumer_sync<CW>();
   }
   const int col = c0 + tid;
   const int hh = min(col / a.head_pitch, H - 1);
@@ -1539,16 +1546,16 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
     const int64_t wbase = (gi / groups_per_chunk) * kGatWChunk;
     if (gi % groups_per_chunk == 0) {
       // softmax weights of edges [beg + wbase, +kGatWChunk) for all heads
-      consumer_sync();
+      consumer_sync<CW>();
       const int64_t e0 = beg + wbase;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kGatWChunk), end - e0));
-      for (int t = tid; t < cnt; t += kConsumers) {
+      for (int t = tid; t < cnt; t += (CW * 32)) {
         const int64_t u = a.ra.map(a.ra.indices[e0 + t]);
         for (int h = 0; h < H; ++h)
           w_sm[t * H + h] = expf(
               __fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + u * H + h), s_sd[h]), a.slope), s_pk[h]));
       }
-      consumer_sync();
+      consumer_sync<CW>();
     }
     const int g = static_cast<int>(gi % kHubGroups);
     const uint32_t round = static_cast<uint32_t>(gi / kHubGroups);
@@ -1591,11 +1598,13 @@ __global__ void __launch_bounds__(kHubThreads) gat_hub_ring_kernel(GatArgs a, in
   }
 }
 
-int launch_gat_hub_ring(const GatArgs& a, cudaStream_t s) {
+template <int CW>
+int launch_gat_hub_ring_cw(const GatArgs& a, cudaStream_t s) {
+  constexpr int kSlice = 32 * CW;
   const int zw = a.heads * a.head_pitch;
-  const int width = std::min(kHubSlice, zw);
+  const int width = std::min(kSlice, zw);
   const int slice_floats = ((width + 3) / 4) * 4;
-  const int col_blocks = static_cast<int>(ceil_div(zw, kHubSlice));
+  const int col_blocks = static_cast<int>(ceil_div(zw, kSlice));
   int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
   per_group = std::max(1, std::min(per_group, 32));
   // weight chunks must cover whole ring groups
@@ -1603,14 +1612,27 @@ int launch_gat_hub_ring(const GatArgs& a, cudaStream_t s) {
   const int smem = per_group * kHubGroups * slice_floats * 4 + kGatWChunk * a.heads * 4;
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(gat_hub_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GLINT_CUDA(cudaFuncSetAttribute(gat_hub_ring_kernel<CW>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kHubRingBytes + kGatWChunk * kMaxHeads * 4));
     configured = true;
   }
   const int64_t grid = a.sc.n_hub * col_blocks;
-  gat_hub_ring_kernel<<<static_cast<unsigned>(grid), kHubThreads, smem, s>>>(
-      a, per_group, slice_floats, col_blocks, tuning(GLINT_TUNE_HUB_INLINE) == 3);
+  // TMA bulk copies by default (one 512 B request per source row slice;
+  // measured 25.6 vs 26.3 ms LDGSTS at 4x64 and 21.0 vs 22.3 at 4x47,
+  // profiles/r01_gat_sweep.jsonl); knob GLINT_TUNE_HUB_INLINE = 2: LDGSTS
+  const bool bulk = tuning(GLINT_TUNE_HUB_INLINE) != 2;
+  gat_hub_ring_kernel<CW><<<static_cast<unsigned>(grid), (CW + 1) * 32, smem, s>>>(
+      a, per_group, slice_floats, col_blocks, bulk);
   return launch_status("gat_aggregate_hub");
+}
+
+// GAT hub rows: 128-column slices by default (the softmax weights, index
+// stream and per-request cost are shared by more columns than with 64);
+// knob GLINT_TUNE_HUB_INLINE = 4 selects 64-column slices, 1 the register path.
+int launch_gat_hub_ring(const GatArgs& a, cudaStream_t s) {
+  if (tuning(GLINT_TUNE_HUB_INLINE) == 4) return launch_gat_hub_ring_cw<2>(a, s);
+  return launch_gat_hub_ring_cw<4>(a, s);
 }
 
 // Regular rows (schedule entries n_hub..n_rows), LPR lanes per row.
@@ -1639,19 +1661,22 @@ template <int H, int LPR, int VPL, int U, int MINB, int R = 0>
 int launch_gat(const GatArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
   const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
+  const bool after = tuning(GLINT_TUNE_HUB_AFTER) == 1;
+  auto launch_hubs = [&](cudaStream_t hs) -> int {
+    if (tuning(GLINT_TUNE_HUB_INLINE) == 1) {   // one-CTA-per-row register path
+      gat_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, hs>>>(a);
+      return launch_status("gat_aggregate_hub");
+    }
+    return launch_gat_hub_ring(a, hs);
+  };
   SideStream* ss = nullptr;
-  if (a.sc.hub_ctas > 0) {
+  if (a.sc.hub_ctas > 0 && !after) {
     // hub CTAs on the library side stream, concurrent with the regular rows
     int rc = side_stream(&ss);
     if (rc) return rc;
     GLINT_CUDA(cudaEventRecord(ss->fork, s));
     GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-    if (tuning(GLINT_TUNE_HUB_INLINE) == 1) {   // diagnostics: one-CTA-per-row register path
-      gat_hub_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, ss->stream>>>(a);
-      rc = launch_status("gat_aggregate_hub");
-    } else {
-      rc = launch_gat_hub_ring(a, ss->stream);
-    }
+    rc = launch_hubs(ss->stream);
     if (rc) return rc;
     GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   }
@@ -1668,7 +1693,9 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
     if (grid > 0)
       gat_async_kernel<H, LPR, VPL, R, MINB><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   }
-  const int rc = launch_status("gat_aggregate");
+  int rc = launch_status("gat_aggregate");
+  if (rc) return rc;
+  if (a.sc.hub_ctas > 0 && after) return launch_hubs(s);
   if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
   return rc;
 }

@@ -244,7 +244,7 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     s_dst = torch.randn((n, heads), device="cuda")
     sched, nh = kernels.degree_schedule(indptr, None, 0, n)
     outs = []
-    for inline, act in ((0, 0), (1, 0), (0, 1), (3, 0)):
+    for inline, act in ((0, 0), (1, 0), (0, 1), (3, 0), (2, 0), (4, 0)):
         _lib.call("glint_set_tuning", 2, inline)
         out = torch.empty((n, heads * dh), device="cuda")
         kernels.gat_aggregate(out, Z, s_src, s_dst, heads, dh, indptr, indices, n,
@@ -255,6 +255,7 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(torch.relu(outs[0]), outs[2])
     assert torch.equal(outs[0], outs[3])
+    assert torch.equal(outs[0], outs[4]) and torch.equal(outs[0], outs[5])
     # and the same bytes without any hub path (every row in the regular kernel),
     # for every launch variant (register-staged and cp.async ring)
     try:

@@ -133,6 +133,13 @@ def main():
                                   "GBps": agg_bytes(d, e_r, size) / ms / 1e6}), flush=True)
             _lib.call("glint_set_tuning", 2, 0)
             pos += size
+        _lib.call("glint_set_tuning", 8, 1)   # hub rows after the regular rows
+        ms = timed(lambda: kernels.spmm_mean(out, h, g.indptr, g.indices, n, schedule=sched,
+                                             n_hub=hub_pre), args.reps)
+        _lib.call("glint_set_tuning", 8, 0)
+        print(json.dumps({"kernel": "spmm_mean_hubs_after", "dim": d, "ms": ms,
+                          "GBps": agg_bytes(d, g.num_edges, n) / ms / 1e6,
+                          "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
         # register hub kernel: k CTAs per SM, persistent (0 = one CTA per hub unit)
         for per_sm in (1, 2, 4, 0):
             _lib.call("glint_set_tuning", 6, per_sm)
@@ -202,6 +209,16 @@ def sweep_gat(args, g, n):
             print(json.dumps({"kernel": "gat_aggregate", "heads": heads, "head_dim": dh,
                               "variant": variant, "ms": ms, "GBps": nb / ms / 1e6,
                               "identical_to_v0": same}), flush=True)
+        _lib.call("glint_set_tuning", 8, 1)   # hub rows after the regular rows
+        for hub_knob in (0, 4, 1):
+            _lib.call("glint_set_tuning", 2, hub_knob)
+            ms = timed(run, args.reps)
+            print(json.dumps({"kernel": "gat_aggregate_hubs_after", "heads": heads,
+                              "head_dim": dh, "hub_knob": hub_knob, "ms": ms,
+                              "GBps": agg_bytes(heads * hp, g.num_edges, n, heads=heads) / ms / 1e6,
+                              "identical_to_v0": bool(torch.equal(ref, out))}), flush=True)
+        _lib.call("glint_set_tuning", 2, 0)
+        _lib.call("glint_set_tuning", 8, 0)
         for hub_knob in (1, 3):         # hub rows: register CTAs / TMA ring (default: LDGSTS ring)
             _lib.call("glint_set_tuning", 3, 0)
             _lib.call("glint_set_tuning", 2, hub_knob)
