@@ -65,18 +65,32 @@ typedef void* glint_stream_t; /* cudaStream_t */
 const char* glint_last_error(void);
 int glint_abi_version(void);
 
-/* Process-wide tuning knobs (performance only; results are identical for
- * every setting).  0 selects the default. */
-#define GLINT_TUNE_MEAN_VARIANT 0 /* K1 launch variant (occupancy / unroll) */
-#define GLINT_TUNE_GEMM_PROF 1    /* 1: K2 tcgen05 kernel accumulates phase cycles */
-#define GLINT_TUNE_HUB_INLINE 2   /* K1 hub rows: 0 auto, 1 register path in the main
-                                     kernel, 2 bulk-copy kernel on a side stream */
-#define GLINT_TUNE_GAT_VARIANT 3  /* K4 launch variant (occupancy / unroll) */
-#define GLINT_TUNE_GEMM_V1 4      /* 1: K2 uses the single-accumulator tcgen05 kernel */
-#define GLINT_TUNE_GEMM_RAWHI 5   /* experiment: unmasked fp32 as the tf32 "hi" operand */
-#define GLINT_TUNE_HUB_CTAS_PER_SM 6 /* K1 register hub kernel: k > 0 caps it at k CTAs per SM */
-#define GLINT_TUNE_GEMM_WIDE 7    /* K2, N in (128, 256]: 0 = 128 x N tiles, 2 = 256 x N/2 tiles */
-#define GLINT_TUNE_HUB_AFTER 8     /* hub-row kernels: 0 concurrent (side stream), 1 after the regular rows */
+/* Process-wide tuning knobs.  0 selects the measured default everywhere.
+ * Performance knobs never change results (every setting is byte-checked
+ * against the default in tests/test_kernels_gpu.py); the two DIAGNOSTIC
+ * settings marked below produce wrong numbers on purpose and exist only for
+ * tools/sweep_kernels.py. */
+#define GLINT_TUNE_MEAN_VARIANT 0 /* K1 regular-row variant: 0 default (cp.async ring),
+                                     1-6 register-staged, 7-15 other ring shapes */
+#define GLINT_TUNE_GEMM_PROF 1    /* K2: 1 phase-cycle counters (v1); DIAGNOSTIC 2 MMA
+                                     issue only, 3 no lo pass (v2) */
+#define GLINT_TUNE_HUB_INLINE 2   /* hub-row path.  K1: 0 auto (ring CTAs < 2^19 rows,
+                                     else register CTAs), 1 register CTAs, 2 LDGSTS
+                                     ring 32 cols, 3 TMA ring 32 cols, 4 LDGSTS ring
+                                     64 cols, 5 one-warp cp.async units.  K4: 0 TMA
+                                     ring 128 cols, 1 register CTAs, 2 LDGSTS ring
+                                     128 cols, 4 TMA ring 64 cols */
+#define GLINT_TUNE_GAT_VARIANT 3  /* K4 regular-row variant (0 default; 5-8 cp.async
+                                     ring; two-phase path 1-3) */
+#define GLINT_TUNE_GEMM_V1 4      /* 1: K2 uses the v1 single-accumulator kernel */
+#define GLINT_TUNE_GEMM_RAWHI 5   /* v1 only: the unmasked fp32 word as the tf32 "hi"
+                                     operand (the truncation probe) */
+#define GLINT_TUNE_HUB_CTAS_PER_SM 6 /* K1 register hub kernel: k > 0 caps it at k CTAs
+                                        per SM (persistent) */
+#define GLINT_TUNE_GEMM_WIDE 7    /* K2: N in (128, 256] 0 = 128 x N tiles, 2 = 256 x
+                                     N/2; N <= 128: 3 = 128-row tiles */
+#define GLINT_TUNE_HUB_AFTER 8    /* hub-row kernels: 0 concurrent (side stream), 1 after
+                                     the regular rows on the caller's stream */
 #define GLINT_TUNE_COUNT 12
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
