@@ -51,6 +51,10 @@ struct RowAddr {
   __device__ __forceinline__ int64_t map(int64_t u) const {
     return col_map ? static_cast<int64_t>(col_map[u]) : u;
   }
+  // 32-bit form for the hot loops (ids and mapped rows are < 2^31)
+  __device__ __forceinline__ int32_t map32(int32_t u) const {
+    return col_map ? __ldg(col_map + u) : u;
+  }
   __device__ __forceinline__ int64_t self_row(int64_t r, int64_t rid) const {
     return self_rows ? self_rows[r] : map(rid);
   }
@@ -510,6 +514,8 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   for (int k = 0; k < VPL; ++k) ok[k] = col0 + (lane_g + LPR * k) * 4 < a.dim;
   const uint32_t ring_s = smem_u32(ring);
 
+  const float* hbase = a.h + col0 + lane_g * 4;
+  const int32_t ld32 = static_cast<int32_t>(a.ld_h);
   // issue cursor: edge `ie`, index chunk [cb, cb+LPR) held in `cur`, next in `nxt`
   int ie = 0, cb = 0;
   int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
@@ -520,8 +526,8 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
       cur = nxt;
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
     }
-    const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
-    const float* src = a.h + u * a.ld_h + col0 + lane_g * 4;
+    const int32_t u = a.ra.map32(__shfl_sync(gmask, cur, ie - cb, LPR));
+    const float* src = hbase + static_cast<int64_t>(u) * ld32;   // one IMAD.WIDE
 #pragma unroll
     for (int k = 0; k < VPL; ++k)
       if (ok[k])
@@ -1821,6 +1827,7 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
   GLINT_REQUIRE(dim > 0, "spmm_mean: dim must be > 0");
   GLINT_REQUIRE(indptr && h && out, "spmm_mean: null indptr/h/out");
   GLINT_REQUIRE(ld_h >= dim && ld_out >= dim, "spmm_mean: leading dimension < dim");
+  GLINT_REQUIRE(ld_h < (1LL << 31), "spmm_mean: ld_h must be < 2^31");
   GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows, "spmm_mean: n_hub out of range");
   GLINT_REQUIRE(schedule || n_hub == 0, "spmm_mean: hub rows need a schedule");
   GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "spmm_mean: bad act %d", act);
