@@ -142,13 +142,14 @@ __device__ __forceinline__ void mean_row_regular(const MeanArgs& a, int64_t r, i
     int32_t nxt = (beg + lane_g < end) ? __ldg(a.ra.indices + beg + lane_g) : 0;
     for (int64_t e0 = beg; e0 < end; e0 += LPR) {
       const int cnt = static_cast<int>(min(static_cast<int64_t>(LPR), end - e0));
-      const int64_t my = (lane_g < cnt) ? a.ra.map(nxt) * a.ld_h : 0;
+      const int32_t my = (lane_g < cnt) ? a.ra.map32(nxt) : 0;
       if (e0 + LPR + lane_g < end) nxt = __ldg(a.ra.indices + e0 + LPR + lane_g);
       for (int j = 0; j < cnt; j += U) {
         float v[U][VPL][VEC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int64_t off = shfl64(gmask, my, (j + u) & (LPR - 1), LPR);
+          const int64_t off = static_cast<int64_t>(__shfl_sync(gmask, my, (j + u) & (LPR - 1), LPR)) *
+                              static_cast<int32_t>(a.ld_h);
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
             const int col = c0 + (lane_g + LPR * k) * VEC;
@@ -971,21 +972,23 @@ __device__ __forceinline__ void gat_row_regular(const GatArgs& a, int64_t r, int
 
   for (int64_t e0 = beg; e0 < end; e0 += LPR) {
     const int cnt = static_cast<int>(min(static_cast<int64_t>(LPR), end - e0));
-    int64_t my = 0;
+    int32_t my = 0;   // source row id (ids and rows < 2^31): one shuffle per edge
     if (lane_g < cnt) {
-      const int64_t u = a.ra.map(a.ra.indices[e0 + lane_g]);
-      my = u * a.ldz;
+      const int32_t u = a.ra.map32(a.ra.indices[e0 + lane_g]);
+      my = u;
 #pragma unroll
       for (int h = 0; h < H; ++h)
-        w_s[lane_g * H + h] = expf(
-            __fsub_rn(leaky(__fadd_rn(__ldg(a.s_src + u * H + h), st[h]), a.slope), st[H + h]));
+        w_s[lane_g * H + h] = expf(__fsub_rn(
+            leaky(__fadd_rn(__ldg(a.s_src + static_cast<int64_t>(u) * H + h), st[h]), a.slope),
+            st[H + h]));
     }
     __syncwarp(gmask);
     for (int j = 0; j < cnt; j += U) {
       float4 v[U][VPL];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t off = shfl64(gmask, my, (j + u) & (LPR - 1), LPR);
+        const int64_t off = static_cast<int64_t>(__shfl_sync(gmask, my, (j + u) & (LPR - 1), LPR)) *
+                            static_cast<int32_t>(a.ldz);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
           const int zc = (lane_g + LPR * k) * 4;
@@ -1905,6 +1908,7 @@ int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim, 
   GLINT_REQUIRE(heads >= 1 && heads <= kMaxHeads, "gat_aggregate: heads must be in [1, %d]", kMaxHeads);
   GLINT_REQUIRE(head_dim >= 1 && head_pitch >= head_dim && head_pitch % 4 == 0,
                 "gat_aggregate: head_pitch must be a multiple of 4 and >= head_dim");
+  GLINT_REQUIRE(ldz < (1LL << 31), "gat_aggregate: ldz must be < 2^31");
   GLINT_REQUIRE(ldz % 4 == 0 && ldz >= static_cast<int64_t>(heads) * head_pitch && aligned16(Z),
                 "gat_aggregate: Z must be 16B aligned with ldz %% 4 == 0 and ldz >= heads*head_pitch");
   GLINT_REQUIRE(indptr && Z && s_src && s_dst && out, "gat_aggregate: null argument");
