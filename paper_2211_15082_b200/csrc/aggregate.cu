@@ -1108,43 +1108,72 @@ __device__ __forceinline__ void gat_row_hub(const GatArgs& a, int64_t r, int col
   }
 }
 
-// Regular GAT row through a per-lane cp.async ring (as mean_row_async): lane
-// g owns the 16-byte Z chunks g, g+LPR, ...; per edge it copies its chunks AND
-// the source score s_src[u, head(chunk)] (4 bytes) into ring slot (edge % R),
-// R-1 edges ahead, and at consume time turns the score into the softmax
-// weight itself -- the same expression as gat_row_regular's, so the bytes
-// match it; accumulation in stored edge order, self last.
+// H per-head scores of one node (s_src / s_dst rows are H floats): one vector
+// load when the table is aligned for it (vec, warp-uniform).
+template <int H>
+struct Scores {
+  float v[H];
+};
+
+template <int H>
+__device__ __forceinline__ Scores<H> load_scores(const float* __restrict__ p, bool vec) {
+  Scores<H> s;
+  if (H == 4 && vec) {
+    const float4 t = ldg_f4(p);
+    s.v[0] = t.x; s.v[1] = t.y; s.v[2 % H] = t.z; s.v[3 % H] = t.w;
+  } else if (H == 2 && vec) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    s.v[0] = t.x; s.v[1 % H] = t.y;
+  } else {
+#pragma unroll
+    for (int h = 0; h < H; ++h) s.v[h] = __ldg(p + h);
+  }
+  return s;
+}
+
+// Regular GAT row through a per-lane cp.async ring (as mean_row_async) -- the
+// Z bytes stream continuously with R-1 edges in flight, while the softmax
+// weights are computed once per edge and head, a chunk of LPR edges at a time:
+//   pass 1: per-head peak over self + edges (order-free max, vector score loads);
+//   pass 2: lane g owns the 16-byte Z chunks g, g+LPR, ... and issues them for
+//           edge ie into ring slot (ie % R).  When the issue cursor enters edge
+//           chunk c, lane i loads the H source scores of edge c*LPR+i into
+//           registers; R edges later, when consumption enters chunk c, it
+//           turns them into the chunk's weights wbuf[i][h] (the expression of
+//           gat_row_regular) -- R <= LPR keeps one chunk of weights live.
+// Accumulation: den += w; num += w*z in stored edge order, self last, so the
+// bytes equal gat_row_regular's.
 template <int H, int LPR, int VPL, int R>
 __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int lane_g,
-                                              unsigned gmask, float4* zring, float* sgrp) {
-  // sgrp: this group's score slots, slot t at sgrp[t * 32 + h]
+                                              unsigned gmask, float4* zring, float* wbuf) {
+  static_assert(R <= LPR, "one chunk of weights is live at a time");
   const int64_t rid = a.ra.csr_row(r);
   const int64_t beg = a.ra.indptr[rid];
   const int64_t end = a.ra.indptr[rid + 1];
   const int64_t self = a.ra.self_row(r, rid);
   const int deg = static_cast<int>(end - beg);
+  const bool vec = (reinterpret_cast<uintptr_t>(a.s_src) % (4 * H) == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.s_dst) % (4 * H) == 0);
 
-  // pass 1: per-head peak over self + edges (order-free), two index loads in flight
-  float sd_k[VPL], pk_k[VPL];
-  int hk[VPL];
-  bool ok[VPL];
+  float sdst[H], peak[H];
   {
-    float sdst[H], peak[H];
+    const Scores<H> sd = load_scores<H>(a.s_dst + self * H, vec);
+    const Scores<H> ss = load_scores<H>(a.s_src + self * H, vec);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      sdst[h] = __ldg(a.s_dst + self * H + h);
-      peak[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sdst[h]), a.slope);
+      sdst[h] = sd.v[h];
+      peak[h] = leaky(__fadd_rn(ss.v[h], sdst[h]), a.slope);
     }
     for (int e = lane_g; e < deg; e += 2 * LPR) {
-      const int64_t u0 = a.ra.map(a.ra.indices[beg + e]);
       const bool two = e + LPR < deg;
-      const int64_t u1 = two ? a.ra.map(a.ra.indices[beg + e + LPR]) : u0;
+      const int32_t u0 = a.ra.map32(__ldg(a.ra.indices + beg + e));
+      const int32_t u1 = two ? a.ra.map32(__ldg(a.ra.indices + beg + e + LPR)) : u0;
+      const Scores<H> s0 = load_scores<H>(a.s_src + static_cast<int64_t>(u0) * H, vec);
+      const Scores<H> s1 = load_scores<H>(a.s_src + static_cast<int64_t>(u1) * H, vec);
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const float s0 = __ldg(a.s_src + u0 * H + h);
-        const float s1 = __ldg(a.s_src + u1 * H + h);
-        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s0, sdst[h]), a.slope));
-        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s1, sdst[h]), a.slope));
+        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s0.v[h], sdst[h]), a.slope));
+        peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s1.v[h], sdst[h]), a.slope));
       }
     }
 #pragma unroll
@@ -1153,31 +1182,32 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       for (int o = LPR / 2; o > 0; o >>= 1)
         peak[h] = fmaxf(peak[h], __shfl_xor_sync(gmask, peak[h], o, LPR));
     }
+  }
+  bool ok[VPL];
+  int hk[VPL];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const int zc = (lane_g + LPR * k) * 4;
-      ok[k] = zc < H * a.head_pitch;
-      hk[k] = ok[k] ? zc / a.head_pitch : 0;
-      sd_k[k] = sdst[0];
-      pk_k[k] = peak[0];
-#pragma unroll
-      for (int h = 1; h < H; ++h)
-        if (h == hk[k]) { sd_k[k] = sdst[h]; pk_k[k] = peak[h]; }
-    }
+  for (int k = 0; k < VPL; ++k) {
+    const int zc = (lane_g + LPR * k) * 4;
+    ok[k] = zc < H * a.head_pitch;
+    hk[k] = ok[k] ? zc / a.head_pitch : 0;
   }
 
-  const uint32_t zr = smem_u32(zring), sr = smem_u32(sgrp);
+  const uint32_t zr = smem_u32(zring);
   int ie = 0, cb = 0;
-  int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
+  int32_t ucur = (lane_g < deg) ? a.ra.map32(__ldg(a.ra.indices + beg + lane_g)) : 0;
   int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
+  Scores<H> sc;                                     // scores of this lane's edge in chunk cb
+  if (lane_g < deg) sc = load_scores<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec);
   auto issue = [&](int slot) {
     if (ie - cb == LPR) {
       cb += LPR;
-      cur = nxt;
+      ucur = a.ra.map32(nxt);
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
+      if (cb + lane_g < deg) sc = load_scores<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec);
     }
-    const int64_t u = a.ra.map(__shfl_sync(gmask, cur, ie - cb, LPR));
-    const float* zsrc = a.Z + u * a.ldz + lane_g * 4;
+    const int64_t off = static_cast<int64_t>(__shfl_sync(gmask, ucur, ie - cb, LPR)) *
+                        static_cast<int32_t>(a.ldz);
+    const float* zsrc = a.Z + off + lane_g * 4;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
@@ -1185,10 +1215,6 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
         cp_async16(zr + o * 16u, zsrc + LPR * 4 * k);
       }
     }
-    if (lane_g < H)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
-                   ::"r"(sr + static_cast<uint32_t>(slot * 32 + lane_g) * 4u), "l"(a.s_src + u * H + lane_g)
-                   : "memory");
     ++ie;
   };
 
@@ -1204,17 +1230,23 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
     if (ie < deg) issue(t);
     cp_async_commit();
   }
-  int slot = 0;
+  int slot = 0, jc = 0;
   for (int j = 0; j < deg; ++j) {
+    if (jc == 0) {   // consumption enters a chunk: its weights from the staged scores
+      if (j + lane_g < deg) {
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          wbuf[lane_g * H + h] =
+              expf(__fsub_rn(leaky(__fadd_rn(sc.v[h], sdst[h]), a.slope), peak[h]));
+      }
+    }
     cp_async_wait<R - 1>();
-    __syncwarp(gmask);   // the group's score copies for this edge have landed
+    __syncwarp(gmask);   // ring slot landed; the chunk's weights are visible
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
-        const int o = (slot * VPL + k) * kThreads;
-        const float4 v = zring[o];
-        const float w = expf(__fsub_rn(leaky(__fadd_rn(sgrp[slot * 32 + hk[k]], sd_k[k]), a.slope),
-                                       pk_k[k]));
+        const float4 v = zring[(slot * VPL + k) * kThreads];
+        const float w = wbuf[jc * H + hk[k]];
         den[k] = __fadd_rn(den[k], w);
         num[k][0] = __fadd_rn(num[k][0], __fmul_rn(w, v.x));
         num[k][1] = __fadd_rn(num[k][1], __fmul_rn(w, v.y));
@@ -1222,27 +1254,35 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
         num[k][3] = __fadd_rn(num[k][3], __fmul_rn(w, v.w));
       }
     }
-    __syncwarp(gmask);   // every lane is done with the slot before it is refilled
+    __syncwarp(gmask);   // every lane is done with the slot (and the chunk) before refills
     if (ie < deg) issue(slot);
     cp_async_commit();
     slot = (slot + 1 == R) ? 0 : slot + 1;
+    jc = (jc + 1 == LPR) ? 0 : jc + 1;
   }
   cp_async_wait<0>();
+  {   // self weights (one per head) through the chunk-weight buffer
+    const Scores<H> ssf = load_scores<H>(a.s_src + self * H, vec);
+    __syncwarp(gmask);
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      if (lane_g == h) wbuf[h] = expf(__fsub_rn(leaky(__fadd_rn(ssf.v[h], sdst[h]), a.slope), peak[h]));
+    __syncwarp(gmask);
+  }
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     if (!ok[k]) continue;
     const int zc = (lane_g + LPR * k) * 4;
     const int hh = hk[k];
-    const int jc = zc - hh * a.head_pitch;
+    const int jcol = zc - hh * a.head_pitch;
     const float4 zs = ldg_f4(a.Z + self * a.ldz + zc);
-    const float ws = expf(__fsub_rn(
-        leaky(__fadd_rn(__ldg(a.s_src + self * H + hh), sd_k[k]), a.slope), pk_k[k]));
+    const float ws = wbuf[hh];
     const float d = __fadd_rn(den[k], ws);
     const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
-    float* dst = a.out + r * a.ld_out + hh * a.head_dim + jc;
+    float* dst = a.out + r * a.ld_out + hh * a.head_dim + jcol;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (jc + c < a.head_dim)
+      if (jcol + c < a.head_dim)
         dst[c] = gat_epilogue(a, __fdiv_rn(__fadd_rn(num[k][c], __fmul_rn(ws, zv[c])), d));
   }
 }
@@ -1260,8 +1300,8 @@ __global__ void __launch_bounds__(kThreads, MINB) gat_async_kernel(GatArgs a) {
   if (idx >= a.sc.n_rows) return;
   const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
   const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
-  float* sbase = reinterpret_cast<float*>(gring + R * VPL * kThreads) + warp * R * 32 + group * LPR;
-  gat_row_async<H, LPR, VPL, R>(a, r, lane_g, gmask, gring + threadIdx.x, sbase);
+  float* wbuf = reinterpret_cast<float*>(gring + R * VPL * kThreads) + (warp * 32 + group * LPR) * H;
+  gat_row_async<H, LPR, VPL, R>(a, r, lane_g, gmask, gring + threadIdx.x, wbuf);
 }
 
 // ------------------------------------------------ two-phase GAT (SDDMM + SpMM) --
@@ -1692,7 +1732,7 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
   if constexpr (R == 0) {
     if (grid > 0) gat_kernel<H, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
   } else {
-    constexpr int smem = R * VPL * kThreads * 16 + R * kThreads * 4;  // Z chunks + group scores
+    constexpr int smem = R * VPL * kThreads * 16 + kThreads * H * 4;  // Z ring + chunk weights
     static bool configured = false;
     if (!configured) {
       GLINT_CUDA(cudaFuncSetAttribute(gat_async_kernel<H, LPR, VPL, R, MINB>,
@@ -1773,27 +1813,29 @@ int dispatch_gat_h(const GatArgs& a, int chunks, cudaStream_t s) {
     if (v == 5) return launch_gat<H, 32, 1, 0, 4, 8>(a, s);
     return launch_gat<H, 32, 1, 4, 6>(a, s);
   }
-  if (chunks <= 48) {
-    if (v == 1) return launch_gat<H, 16, 3, 3, 3>(a, s);
+  if (chunks <= 48) {   // 0 and 5-9: cp.async ring (R <= LPR); 1-4: register-staged
+    if (v == 1) return launch_gat<H, 16, 3, 2, 4>(a, s);
     if (v == 2) return launch_gat<H, 32, 2, 3, 4>(a, s);
-    if (v == 3) return launch_gat<H, 16, 3, 2, 5>(a, s);
-    if (v == 4) return launch_gat<H, 16, 3, 2, 4>(a, s);
-    if (v == 5) return launch_gat<H, 16, 3, 0, 3, 6>(a, s);
-    if (v == 6) return launch_gat<H, 16, 3, 0, 4, 4>(a, s);
-    if (v == 7) return launch_gat<H, 32, 2, 0, 4, 6>(a, s);
-    if (v == 8) return launch_gat<H, 32, 2, 0, 3, 8>(a, s);
-    return launch_gat<H, 16, 3, 2, 4>(a, s);
+    if (v == 3) return launch_gat<H, 16, 3, 3, 3>(a, s);
+    if (v == 4) return launch_gat<H, 16, 3, 2, 5>(a, s);
+    if (v == 5) return launch_gat<H, 16, 3, 0, 4, 4>(a, s);
+    if (v == 6) return launch_gat<H, 16, 3, 0, 5, 3>(a, s);
+    if (v == 7) return launch_gat<H, 16, 3, 0, 3, 6>(a, s);
+    if (v == 8) return launch_gat<H, 32, 2, 0, 4, 4>(a, s);
+    if (v == 9) return launch_gat<H, 16, 3, 0, 4, 2>(a, s);
+    return launch_gat<H, 16, 3, 0, 4, 3>(a, s);
   }
   if (chunks <= 64) {
-    if (v == 1) return launch_gat<H, 32, 2, 4, 3>(a, s);
-    if (v == 2) return launch_gat<H, 32, 2, 2, 5>(a, s);
-    if (v == 3) return launch_gat<H, 32, 2, 4, 4>(a, s);
-    if (v == 4) return launch_gat<H, 32, 2, 3, 5>(a, s);
-    if (v == 5) return launch_gat<H, 32, 2, 0, 4, 4>(a, s);
-    if (v == 6) return launch_gat<H, 32, 2, 0, 3, 6>(a, s);
-    if (v == 7) return launch_gat<H, 32, 2, 0, 4, 6>(a, s);
-    if (v == 8) return launch_gat<H, 32, 2, 0, 3, 8>(a, s);
-    return launch_gat<H, 32, 2, 3, 4>(a, s);
+    if (v == 1) return launch_gat<H, 32, 2, 3, 4>(a, s);
+    if (v == 2) return launch_gat<H, 32, 2, 4, 3>(a, s);
+    if (v == 3) return launch_gat<H, 32, 2, 2, 5>(a, s);
+    if (v == 4) return launch_gat<H, 32, 2, 4, 4>(a, s);
+    if (v == 5) return launch_gat<H, 32, 2, 0, 4, 3>(a, s);
+    if (v == 6) return launch_gat<H, 32, 2, 0, 5, 3>(a, s);
+    if (v == 7) return launch_gat<H, 32, 2, 0, 4, 2>(a, s);
+    if (v == 8) return launch_gat<H, 32, 2, 0, 5, 4>(a, s);
+    if (v == 9) return launch_gat<H, 32, 2, 0, 3, 6>(a, s);
+    return launch_gat<H, 32, 2, 0, 4, 4>(a, s);
   }
   if (chunks <= 128) return launch_gat<H, 32, 4, 2, 3>(a, s);
   return launch_gat<H, 32, 8, 1, 2>(a, s);

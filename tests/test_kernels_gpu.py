@@ -259,7 +259,7 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     # and the same bytes without any hub path (every row in the regular kernel),
     # for every launch variant (register-staged and cp.async ring)
     try:
-        for v in range(9):
+        for v in range(10):
             _lib.call("glint_set_tuning", 3, v)
             plain = torch.empty_like(outs[0])
             kernels.gat_aggregate(plain, Z, s_src, s_dst, heads, dh, indptr, indices, n)
