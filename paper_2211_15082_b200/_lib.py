@@ -10,12 +10,15 @@ raw CUDA device addresses (``torch.Tensor.data_ptr()``), streams are the raw
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
 from .errors import InternalError
 
 LIB_PATH = pathlib.Path(__file__).resolve().with_name("libglint_b200.so")
+if os.environ.get("GLINT_LIB_PATH"):   # A/B builds of the same library (tools only)
+    LIB_PATH = pathlib.Path(os.environ["GLINT_LIB_PATH"]).resolve()
 HEADER_PATH = pathlib.Path(__file__).resolve().parents[1] / "include" / "glint_b200.h"
 
 GLINT_OK = 0

@@ -510,9 +510,11 @@ int launch_bn(const TcArgs& a, int act, cudaStream_t s) {
 //   * Tiles are 256 rows x BN <= 128 columns; TMEM holds TWO accumulators
 //     (2 x 2 halves x BN <= 512 columns): the MMA warp starts tile i+1 while the
 //     epilogue warps drain tile i.
+#ifndef GLINT_GEMM_RA1
+#define GLINT_GEMM_RA1 8
+#endif
 namespace v2 {
 
-constexpr int RA = 6;   // raw-A ring (cp.async, also the TF32 "hi" operand)
 constexpr int RL = 2;   // A "lo" ring (computed by the producers)
 constexpr int RW = 3;   // W panel ring (TMA bulk copies)
 constexpr int kEpiWarps2 = 8;
@@ -535,6 +537,9 @@ struct Roles {
 template <int BN, int MH = 2>   // MH: 128-row M halves per tile (2: 256 x BN, 1: 128 x BN)
 struct Cfg2 {
   static constexpr int TM = MH * HALF;           // tile rows
+  // raw-A ring (cp.async, also the TF32 "hi" operand): 128-row tiles have the
+  // shared memory for a deeper ring (more loads in flight per SM)
+  static constexpr int RA = MH == 1 ? GLINT_GEMM_RA1 : 6;
   static constexpr int A_BYTES = TM * BK * 4;  // one raw / lo slot (TM x 16 fp32)
   static constexpr int W_BYTES = BN * BK * 4;  // one of W hi / lo
   static constexpr int RAW_OFF = 0;
@@ -690,7 +695,7 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
   using Rl = Roles<MH>;
   constexpr int PER = C::TM * 4 / Rl::PT;   // 16-byte chunks per producer thread
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t raw_empty[RA];
+  __shared__ __align__(8) uint64_t raw_empty[C::RA];
   __shared__ __align__(8) uint64_t lo_full[RL], lo_empty[RL];
   __shared__ __align__(8) uint64_t w_full[RW], w_empty[RW];
   __shared__ __align__(8) uint64_t tmem_full[2];
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < RA; ++i) mbar_init(&raw_empty[i], 1);           // tcgen05.commit
+    for (int i = 0; i < C::RA; ++i) mbar_init(&raw_empty[i], 1);           // tcgen05.commit
     for (int i = 0; i < RL; ++i) {
       mbar_init(&lo_full[i], Rl::PW);                           // one per producer warp
       mbar_init(&lo_empty[i], 1);
@@ -749,8 +754,8 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
     }
     const uint32_t raw_base = smem_addr(smem + C::RAW_OFF);
     auto issue = [&](int64_t idx) {
-      const int slot = static_cast<int>(idx % RA);
-      const uint32_t use = static_cast<uint32_t>(idx / RA);
+      const int slot = static_cast<int>(idx % C::RA);
+      const uint32_t use = static_cast<uint32_t>(idx / C::RA);
       mbar_wait(&raw_empty[slot], (use & 1u) ^ 1u);
       const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
       const int kb = static_cast<int>(idx % nkb);
@@ -766,13 +771,13 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
                      : "memory");
       }
     };
-    for (int64_t d = 0; d < RA - 1; ++d) {
+    for (int64_t d = 0; d < C::RA - 1; ++d) {
       if (d < total) issue(d);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int64_t idx = 0; idx < total; ++idx) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(RA - 2) : "memory");  // own copies of idx landed
-      const int rs = static_cast<int>(idx % RA);
+      asm volatile("cp.async.wait_group %0;" ::"n"(C::RA - 2) : "memory");  // own copies of idx landed
+      const int rs = static_cast<int>(idx % C::RA);
       const int ls = static_cast<int>(idx % RL);
       const uint32_t luse = static_cast<uint32_t>(idx / RL);
       mbar_wait(&lo_empty[ls], (luse & 1u) ^ 1u);
@@ -791,7 +796,7 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&lo_full[ls]);
-      if (idx + RA - 1 < total) issue(idx + RA - 1);
+      if (idx + C::RA - 1 < total) issue(idx + C::RA - 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -821,7 +826,7 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
       fence_after();
       for (int kb = 0; kb < nkb; ++kb) {
         const int64_t idx = it * nkb + kb;
-        const int rs = static_cast<int>(idx % RA);
+        const int rs = static_cast<int>(idx % C::RA);
         const int ls = static_cast<int>(idx % RL);
         const int ws = static_cast<int>(idx % RW);
         if (!a.mma_only) {   // a.mma_only: diagnostics, MMA issue rate without operand waits
@@ -903,11 +908,20 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
         const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(buf * C::ACC + h * BN + cbase);
         ScoreAcc st{-1, 0.0f, 0.0f};
+        if constexpr (SC) {
+          // 16-column chunks: the score chains need registers the 32-wide
+          // chunk would take (96 per thread at 18 warps)
 #pragma unroll 1
-        for (int c0 = 0; c0 + 32 <= CW_SPAN; c0 += 32)
-          epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_s + cbase + c0, has_bias, row_base,
-                                 n0 + cbase + c0, lane, sc_tab, st);
-        if constexpr (CW_SPAN % 32 == 16)
+          for (int c0 = 0; c0 + 16 <= CW_SPAN; c0 += 16)
+            epi_chunk<16, ACT, SC>(a, tbase + c0, stage, bias_s + cbase + c0, has_bias, row_base,
+                                   n0 + cbase + c0, lane, sc_tab, st);
+        } else {
+#pragma unroll 1
+          for (int c0 = 0; c0 + 32 <= CW_SPAN; c0 += 32)
+            epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_s + cbase + c0, has_bias, row_base,
+                                   n0 + cbase + c0, lane, sc_tab, st);
+        }
+        if constexpr (!SC && CW_SPAN % 32 == 16)
           epi_chunk<16, ACT, SC>(a, tbase + (CW_SPAN - 16), stage, bias_s + cbase + CW_SPAN - 16,
                                  has_bias, row_base, n0 + cbase + CW_SPAN - 16, lane, sc_tab, st);
         if constexpr (SC) score_flush(a, st, row_base + lane);
