@@ -17,7 +17,8 @@ def main():
     from paper_2211_15082_b200.storage import CscGraph
 
     n, und = synth.PRODUCTS_NODES, synth.PRODUCTS_UNDIRECTED
-    m = synth.build_gcn(100, 256, 47, 3, seed=0)
+    m = (synth.build_gat(100, 64, 47, 3, heads=4, seed=0) if sys.argv[1:2] == ["gat3"]
+         else synth.build_gcn(100, 256, 47, 3, seed=0))
     g = synth.gen_products_like(n, und, seed=0, device="cuda")
     xt = synth.gen_features_device(n, 100, seed=0)
     ip = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
