@@ -399,6 +399,8 @@ class LayerwiseEngine:
         self.exchange = None            # RowExchange of a distributed run (set by run())
         # output chunks streamed to the host sink (each is bounded by its slowest hub row)
         self.sink_chunks = int(os.environ.get("GLINT_SINK_CHUNKS", "2"))
+        # one launch per full-mode conv layer when the budget admits it
+        self.whole_layer = os.environ.get("GLINT_WHOLE_LAYER", "1") == "1"
 
     # -- helpers ------------------------------------------------------------
 
@@ -655,6 +657,21 @@ class LayerwiseEngine:
         # batch records are untouched.
         spec = {"hi": lo}
         speculate = full and blk.has_conv and gl.upload_in_flight()
+        # Whole-layer run (full mode): when the budget admits the layer's rows
+        # as ONE batch, they run as one launch up front (LPT schedule over every
+        # row, hub rows beside them) instead of the controller's bootstrap
+        # batches (layer 1: 1024, 2048, ... rows, each bounded by its slowest
+        # row).  Row invariance makes the bytes identical; the controller still
+        # plans its batches (records and stats unchanged) and execute() finds
+        # their rows done, exactly as for the upload speculation above.
+        if (self.whole_layer and full and blk.has_conv and hi > lo and devmodel.admit(
+                devmodel.footprint_counts(blk, hi - lo, n_nodes, int(prefix[hi] - prefix[lo]),
+                                          self.dims), self.budget)):
+            if self.probe is not None:
+                self.probe.mark(f"L{layer} whole layer [{lo},{hi})")
+            run_rows(lo, hi, n_nodes)
+            spec["hi"] = hi
+            speculate = True
 
         def execute(plan: _Plan):
             if self.probe is not None:

@@ -87,6 +87,38 @@ def test_outputs_invariant_to_batching_and_order(golden, cuda):
                 assert out.tobytes() == base.tobytes(), (th, order)
 
 
+def test_whole_layer_runs_equal_controller_batches(cuda, monkeypatch):
+    """A full-mode conv layer the budget admits as one batch runs as one launch;
+    the bytes and the stats document (the controller's bootstrap batches) must
+    equal the batch-by-batch execution, for every conv kind, with hub rows."""
+    import torch
+
+    from paper_2211_15082_b200 import synth
+    from paper_2211_15082_b200.batching import Thresholds
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+
+    n = 40_000
+    g = synth.gen_products_like(n, n * 25, seed=5, device="cuda")
+    assert int(g.in_degrees.max()) + 1 >= 512          # hub rows present
+    x = synth.gen_features_device(n, 24, seed=5, device="cuda")
+    models = [synth.build_gcn(24, 64, 7, 3, seed=1),
+              synth.build_gat(24, 16, 7, 2, heads=4, seed=2),
+              synth.build_jknet(24, 32, 7, 3, seed=3),
+              synth.build_appnp(24, 32, 7, k=3, alpha=0.1, seed=4)]
+    for m in models:
+        outs, docs = [], []
+        for whole in ("1", "0"):
+            monkeypatch.setenv("GLINT_WHOLE_LAYER", whole)
+            res = run_inference(m, g, x, budget=DeviceBudget(8 << 30),
+                                thresholds=Thresholds(512, 4096), output="device")
+            outs.append(res.output.clone())
+            docs.append(res.stats.document())
+            assert res.stats.batches > m.depth           # the controller did bootstrap
+        assert torch.equal(outs[0], outs[1]), m
+        assert docs[0] == docs[1]
+
+
 def test_reassociation_and_precision_agree(golden, cuda):
     """Transform-then-aggregate (narrowing ConvMean) and both GEMM precisions
     agree with the aggregate-first fp32 path within 1e-5 (bar 1e-4)."""
