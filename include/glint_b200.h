@@ -326,6 +326,16 @@ int glint_rcmk_host(int64_t num_nodes, const int64_t* indptr,
 int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage_pinned,
                        const int64_t* chunk_edges, int32_t n_chunks, int32_t threads,
                        glint_stream_t copy_stream, void** handle_out);
+/* The same with id_bytes = 3 (node ids < 2^24): ids cross PCIe as 24-bit
+ * little-endian triples (stage_pinned: 3 bytes per edge) into dev_stage
+ * (device, 3 bytes per edge), and a kernel on copy_stream unpacks each chunk
+ * into dst_dev before its event -- 25% fewer bytes on the e2e path's floor.
+ * id_bytes = 4 is glint_upload_start (stage_pinned is int32, dev_stage unused).
+ * An id outside [0, 2^24) fails the chunk with GLINT_EINVAL. */
+int glint_upload_start_packed(const int64_t* src_host, int32_t* dst_dev, uint8_t* stage_pinned,
+                              uint8_t* dev_stage, int32_t id_bytes, const int64_t* chunk_edges,
+                              int32_t n_chunks, int32_t threads, glint_stream_t copy_stream,
+                              void** handle_out);
 int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream);
 int glint_upload_query(void* handle, int32_t chunk);
 int glint_upload_finish(void* handle);

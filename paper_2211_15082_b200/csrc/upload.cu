@@ -10,6 +10,7 @@
 // variable, no GIL held -- ctypes releases it) and then for the event on
 // their stream.
 #include <atomic>
+#include <cstring>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -22,6 +23,7 @@ namespace {
 
 struct Upload {
   std::thread worker;
+  int id_bytes = 4;              // 4: int32 ids; 3: 24-bit ids unpacked on the device
   std::vector<cudaEvent_t> events;
   std::vector<int64_t> bounds;   // K+1 edge offsets
   std::vector<int> queued;       // guarded by mu
@@ -51,6 +53,51 @@ void narrow_parallel(const int64_t* src, int32_t* dst, int64_t n, int threads, i
   for (int64_t c : b) *bad += c;
 }
 
+// 24-bit little-endian packing (ids < 2^24): 3 bytes per id cross PCIe
+// instead of 4.  Thread k packs ids [lo, hi) with 4-byte stores advancing by
+// 3; the last id of a range is written bytewise so no store passes `hi`.
+void pack24_parallel(const int64_t* src, uint8_t* dst, int64_t n, int threads, int64_t* bad) {
+  const int t = (n < (1 << 16)) ? 1 : std::max(1, std::min(threads, 64));
+  std::vector<int64_t> b(t, 0);
+  auto work = [&](int k) {
+    const int64_t lo = n * k / t, hi = n * (k + 1) / t;
+    int64_t c = 0;
+    uint8_t* p = dst + 3 * lo;
+    for (int64_t i = lo; i < hi; ++i, p += 3) {
+      const int64_t v = src[i];
+      c += (v < 0 || v >= (1LL << 24));
+      const uint32_t u = static_cast<uint32_t>(v) & 0xFFFFFFu;
+      if (i + 1 < hi) {
+        std::memcpy(p, &u, 4);    // the 4th byte is overwritten by id i+1
+      } else {
+        p[0] = static_cast<uint8_t>(u);
+        p[1] = static_cast<uint8_t>(u >> 8);
+        p[2] = static_cast<uint8_t>(u >> 16);
+      }
+    }
+    b[k] = c;
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int64_t c : b) *bad += c;
+}
+
+// Device side of the 24-bit upload: 4 ids (12 bytes) per thread.
+__global__ void unpack24_kernel(const uint8_t* __restrict__ src, int32_t* __restrict__ dst,
+                                int64_t n) {
+  const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t i = i0 + j;
+    if (i < n) {
+      const uint8_t* p = src + 3 * i;
+      dst[i] = static_cast<int32_t>(p[0] | (p[1] << 8) | (p[2] << 16));
+    }
+  }
+}
+
 }  // namespace
 }  // namespace glint
 
@@ -58,16 +105,20 @@ using namespace glint;
 
 extern "C" {
 
-int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage_pinned,
-                       const int64_t* chunk_edges, int32_t n_chunks, int32_t threads,
-                       glint_stream_t copy_stream, void** handle_out) {
+static int upload_start(const int64_t* src_host, int32_t* dst_dev, void* stage_pinned,
+                        uint8_t* dev_stage, int id_bytes, const int64_t* chunk_edges,
+                        int32_t n_chunks, int32_t threads, glint_stream_t copy_stream,
+                        void** handle_out) {
   GLINT_REQUIRE(handle_out && n_chunks >= 0 && chunk_edges, "upload_start: bad argument");
-  GLINT_REQUIRE(n_chunks == 0 || (src_host && dst_dev && stage_pinned),
+  GLINT_REQUIRE(id_bytes == 4 || id_bytes == 3, "upload_start: id_bytes must be 3 or 4");
+  GLINT_REQUIRE(n_chunks == 0 || (src_host && dst_dev && stage_pinned &&
+                                  (id_bytes == 4 || dev_stage)),
                 "upload_start: null buffer");
   for (int k = 0; k < n_chunks; ++k)
     GLINT_REQUIRE(chunk_edges[k] <= chunk_edges[k + 1] && chunk_edges[k] >= 0,
                   "upload_start: chunk bounds must be non-decreasing");
   auto* u = new Upload();
+  u->id_bytes = id_bytes;
   GLINT_CUDA(cudaGetDevice(&u->device));
   u->bounds.assign(chunk_edges, chunk_edges + n_chunks + 1);
   u->queued.assign(n_chunks, 0);
@@ -75,18 +126,35 @@ int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage
   for (int k = 0; k < n_chunks; ++k)
     GLINT_CUDA(cudaEventCreateWithFlags(&u->events[k], cudaEventDisableTiming));
   cudaStream_t s = as_stream(copy_stream);
-  u->worker = std::thread([u, src_host, dst_dev, stage_pinned, threads, s]() {
+  u->worker = std::thread([u, src_host, dst_dev, stage_pinned, dev_stage, threads, s]() {
     cudaSetDevice(u->device);
     for (size_t k = 0; k + 1 < u->bounds.size(); ++k) {
       const int64_t e0 = u->bounds[k], e1 = u->bounds[k + 1];
       int err = 0;
       if (e1 > e0) {
         int64_t bad = 0;
-        narrow_parallel(src_host + e0, stage_pinned + e0, e1 - e0, threads, &bad);
-        if (bad) err = GLINT_EINVAL;
-        else if (cudaMemcpyAsync(dst_dev + e0, stage_pinned + e0, (e1 - e0) * sizeof(int32_t),
-                                 cudaMemcpyHostToDevice, s) != cudaSuccess)
-          err = GLINT_ECUDA;
+        if (u->id_bytes == 4) {
+          int32_t* st = static_cast<int32_t*>(stage_pinned);
+          narrow_parallel(src_host + e0, st + e0, e1 - e0, threads, &bad);
+          if (bad) err = GLINT_EINVAL;
+          else if (cudaMemcpyAsync(dst_dev + e0, st + e0, (e1 - e0) * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s) != cudaSuccess)
+            err = GLINT_ECUDA;
+        } else {
+          uint8_t* st = static_cast<uint8_t*>(stage_pinned);
+          pack24_parallel(src_host + e0, st + 3 * e0, e1 - e0, threads, &bad);
+          if (bad) {
+            err = GLINT_EINVAL;
+          } else if (cudaMemcpyAsync(dev_stage + 3 * e0, st + 3 * e0, 3 * (e1 - e0),
+                                     cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            err = GLINT_ECUDA;
+          } else {
+            const int64_t blocks = ceil_div(ceil_div(e1 - e0, 4), 256);
+            unpack24_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_stage + 3 * e0,
+                                                                          dst_dev + e0, e1 - e0);
+            if (cudaGetLastError() != cudaSuccess) err = GLINT_ECUDA;
+          }
+        }
       }
       if (!err && cudaEventRecord(u->events[k], s) != cudaSuccess) err = GLINT_ECUDA;
       {
@@ -106,6 +174,21 @@ int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage
   return GLINT_OK;
 }
 
+int glint_upload_start(const int64_t* src_host, int32_t* dst_dev, int32_t* stage_pinned,
+                       const int64_t* chunk_edges, int32_t n_chunks, int32_t threads,
+                       glint_stream_t copy_stream, void** handle_out) {
+  return upload_start(src_host, dst_dev, stage_pinned, nullptr, 4, chunk_edges, n_chunks, threads,
+                      copy_stream, handle_out);
+}
+
+int glint_upload_start_packed(const int64_t* src_host, int32_t* dst_dev, uint8_t* stage_pinned,
+                              uint8_t* dev_stage, int32_t id_bytes, const int64_t* chunk_edges,
+                              int32_t n_chunks, int32_t threads, glint_stream_t copy_stream,
+                              void** handle_out) {
+  return upload_start(src_host, dst_dev, stage_pinned, dev_stage, id_bytes, chunk_edges, n_chunks,
+                      threads, copy_stream, handle_out);
+}
+
 // Blocks until chunk k's copy is queued, then makes `stream` wait for it.
 int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream) {
   auto* u = static_cast<Upload*>(handle);
@@ -116,7 +199,8 @@ int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream) {
     u->cv.wait(lk, [&] { return u->queued[chunk] != 0; });
     if (u->error) {
       set_error("upload: chunk failed (%s)", u->error == GLINT_EINVAL
-                ? "node ids do not fit int32" : "CUDA copy error");
+                ? (u->id_bytes == 3 ? "node ids do not fit 24 bits" : "node ids do not fit int32")
+                : "CUDA copy error");
       return u->error;
     }
   }

@@ -478,3 +478,64 @@ def test_streaming_graph_loader(tmp_path, cuda):
         q.write_bytes(data)
         with pytest.raises(FormatError):
             load_graph_device(q, chunk_edges=10000)
+
+
+@pytest.mark.parametrize("pack24", ["1", "0"])
+def test_async_csr_upload_equals_host_graph(cuda, monkeypatch, pack24):
+    """DeviceGraph.upload_async (native thread: host narrowing or 24-bit packing,
+    chunked H2D, per-chunk events) lands the same CSR as the host graph, for
+    uniform and geometric chunks and ragged chunk sizes."""
+    import torch
+
+    from paper_2211_15082_b200 import storage
+
+    monkeypatch.setattr(storage, "PACK24", pack24 == "1")
+    if True:
+        rng = np.random.default_rng(7)
+        n = 70_000
+        degs = rng.integers(0, 40, n)
+        degs[:3] = [0, 5000, 1]
+        ptr = np.concatenate([[0], np.cumsum(degs)]).astype(np.int64)
+        idx = rng.integers(0, n, int(ptr[-1])).astype(np.int64)
+        idx[:5] = [n - 1, 0, 65535, 65536, n - 2]
+        g = storage.CscGraph(n, int(ptr[-1]), ptr, idx)
+        copy = torch.cuda.Stream()
+        for chunks, geometric in ((1, False), (5, True), (7, False)):
+            dg = storage.DeviceGraph.upload_async(g, torch.device("cuda"), copy, chunks=chunks,
+                                                  geometric=geometric)
+            dg.wait_rows()
+            torch.cuda.synchronize()
+            assert np.array_equal(dg.indices.cpu().numpy(), idx.astype(np.int32))
+            assert np.array_equal(dg.indptr.cpu().numpy(), ptr)
+            assert not dg.upload_in_flight()
+
+
+def test_packed_upload_rejects_wide_ids(cuda):
+    """glint_upload_start_packed: an id >= 2^24 fails its chunk with EINVAL
+    (the caller only packs when N <= 2^24), ids up to 2^24 - 1 round-trip."""
+    import ctypes
+
+    import torch
+
+    from paper_2211_15082_b200 import _lib
+
+    lib = _lib.load()
+    for ids, ok in (([0, 1, (1 << 24) - 1, 12345, 7], True), ([3, 1 << 24, 5], False)):
+        src = np.asarray(ids, dtype=np.int64)
+        m = len(src)
+        dst = torch.full((m,), -1, dtype=torch.int32, device="cuda")
+        stage = torch.empty(3 * m, dtype=torch.uint8, pin_memory=True)
+        dstage = torch.empty(3 * m, dtype=torch.uint8, device="cuda")
+        edges = np.asarray([0, m], dtype=np.int64)
+        h = ctypes.c_void_p()
+        s = torch.cuda.current_stream()
+        assert lib.glint_upload_start_packed(src.ctypes.data, dst.data_ptr(), stage.data_ptr(),
+                                             dstage.data_ptr(), 3, edges.ctypes.data, 1, 2,
+                                             ctypes.c_void_p(s.cuda_stream), ctypes.byref(h)) == 0
+        rc = lib.glint_upload_wait(h, 0, ctypes.c_void_p(s.cuda_stream))
+        lib.glint_upload_finish(h)
+        torch.cuda.synchronize()
+        if ok:
+            assert rc == 0 and dst.cpu().tolist() == ids
+        else:
+            assert rc != 0 and "24 bits" in _lib.last_error()

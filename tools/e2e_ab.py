@@ -19,7 +19,7 @@ def main():
     from paper_2211_15082_b200.storage import CscGraph
 
     n, und = synth.PRODUCTS_NODES, synth.PRODUCTS_UNDIRECTED
-    model = sys.argv[1] if len(sys.argv) > 1 else "gcn3"
+    model = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "gcn3"
     m = (synth.build_gcn(100, 256, 47, 3, seed=0) if model == "gcn3"
          else synth.build_gat(100, 64, 47, 3, heads=4, seed=0))
     g = synth.gen_products_like(n, und, seed=0, device="cuda")
@@ -33,16 +33,35 @@ def main():
     hg = CscGraph(n, g.num_edges, ip.numpy(), ix.numpy())
     del g, xt
     budget = DeviceBudget(160 << 30)
-    run_inference(m, hg, xh, budget=budget, output="numpy")
-    torch.cuda.synchronize()
-    times = []
+    from paper_2211_15082_b200 import storage
+
+    # --pack24-ab: alternate 24-bit packed and int32 CSR uploads in one process
+    modes = (True, False) if "--pack24-ab" in sys.argv else (storage.PACK24,)
+    times = {mode: [] for mode in modes}
     res = None
-    for _ in range(5):
+    for mode in modes:             # warm-up (pinned staging, allocator) per mode
+        storage.PACK24 = mode
         res = None
-        t0 = time.perf_counter()
         res = run_inference(m, hg, xh, budget=budget, output="numpy")
-        torch.cuda.synchronize()
-        times.append(1e3 * (time.perf_counter() - t0))
+    torch.cuda.synchronize()
+    for _ in range(6 if len(modes) > 1 else 5):
+        for mode in modes:
+            storage.PACK24 = mode
+            res = None
+            t0 = time.perf_counter()
+            res = run_inference(m, hg, xh, budget=budget, output="numpy")
+            torch.cuda.synchronize()
+            times[mode].append(1e3 * (time.perf_counter() - t0))
+    if len(modes) > 1:
+        import numpy as np
+
+        print(json.dumps({"model": model, "ab": "pack24 vs int32 CSR upload",
+                          "pack24_ms": [round(t, 1) for t in times[True]],
+                          "int32_ms": [round(t, 1) for t in times[False]],
+                          "pack24_median": float(np.median(times[True])),
+                          "int32_median": float(np.median(times[False]))}), flush=True)
+        return
+    times = times[modes[0]]
     print(json.dumps({"model": model, "sink_chunks": os.environ.get("GLINT_SINK_CHUNKS", "2"),
                       "host_narrow": os.environ.get("GLINT_HOST_NARROW", "1"),
                       "chunks": os.environ.get("GLINT_UPLOAD_CHUNKS", "default"),
