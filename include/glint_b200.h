@@ -337,6 +337,12 @@ int glint_upload_start_packed(const int64_t* src_host, int32_t* dst_dev, uint8_t
                               int32_t n_chunks, int32_t threads, glint_stream_t copy_stream,
                               void** handle_out);
 int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream);
+/* Row-pitched async copy, any direction (cudaMemcpy2DAsync with
+ * cudaMemcpyDefault): `rows` rows of row_bytes, pitches in bytes.  Used by the
+ * e2e output sink (pitched device store -> dense pinned host rows; reference
+ * run_inference returns the output as a host array, executor.py:481-543). */
+int glint_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                          int64_t row_bytes, int64_t rows, glint_stream_t stream);
 int glint_upload_query(void* handle, int32_t chunk);
 int glint_upload_finish(void* handle);
 /* Host int64 -> int32 narrowing on `threads` CPU threads (host pointers);

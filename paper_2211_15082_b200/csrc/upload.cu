@@ -189,6 +189,23 @@ int glint_upload_start_packed(const int64_t* src_host, int32_t* dst_dev, uint8_t
                       threads, copy_stream, handle_out);
 }
 
+// Row-pitched copy in any direction (cudaMemcpy2DAsync, cudaMemcpyDefault):
+// the e2e output sink streams finished rows of a pitched device store straight
+// into the caller's dense pinned host array, with no device-side repacking.
+int glint_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                          int64_t row_bytes, int64_t rows, glint_stream_t stream) {
+  GLINT_REQUIRE(rows >= 0 && row_bytes >= 0 && dst_pitch >= row_bytes && src_pitch >= row_bytes,
+                "copy_rows_async: bad pitches (dst %lld, src %lld, row %lld)",
+                static_cast<long long>(dst_pitch), static_cast<long long>(src_pitch),
+                static_cast<long long>(row_bytes));
+  if (rows == 0 || row_bytes == 0) return GLINT_OK;
+  GLINT_REQUIRE(dst && src, "copy_rows_async: null pointer");
+  GLINT_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(dst_pitch), src,
+                               static_cast<size_t>(src_pitch), static_cast<size_t>(row_bytes),
+                               static_cast<size_t>(rows), cudaMemcpyDefault, as_stream(stream)));
+  return GLINT_OK;
+}
+
 // Blocks until chunk k's copy is queued, then makes `stream` wait for it.
 int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream) {
   auto* u = static_cast<Upload*>(handle);

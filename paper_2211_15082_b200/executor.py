@@ -645,7 +645,11 @@ class LayerwiseEngine:
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
                                 gat_cache)
                 if sink_store is not None:
+                    if self.probe is not None:
+                        self.probe.mark(f"L{layer} rows [{c0},{c1}) launched")
                     self.sink(sink_store, c0, c1)
+                    if self.probe is not None:
+                        self.probe.mark(f"L{layer} sink [{c0},{c1}) queued")
                 if full and self.exchange is not None and hasattr(self.exchange, "progress"):
                     self.exchange.progress(self, blk, c1)   # overlap: send finished pieces
 
@@ -1221,7 +1225,14 @@ def resolve_budget(budget, resident_bytes=0):
 
 
 class _HostSink:
-    """Streams finished output rows to pinned host memory on a copy stream."""
+    """Streams finished output rows to pinned host memory on a copy stream.
+
+    A pitched store (47 columns in 48-float rows) is first packed into a dense
+    device buffer allocated here, before the run (K5 row copy on the compute
+    stream, ~0.1 ms per 0.46 GB), so each chunk leaves in one 1-D copy at full
+    PCIe rate: a 2-D copy of 188-byte rows runs at 33 GB/s instead of 52
+    (profiles/r01_pcie_copy_rates.jsonl), and no allocation happens in the
+    last layer's loop."""
 
     def __init__(self, n_rows, dim, device):
         import torch
@@ -1229,15 +1240,21 @@ class _HostSink:
         self.host = torch.empty((n_rows, dim), dtype=torch.float32, pin_memory=True)
         self.stream = torch.cuda.Stream(device=device)
         self.device = device
+        self.dense = None
+        if pitch_of(dim) != dim:
+            self.dense = torch.empty((n_rows, dim), dtype=torch.float32, device=device)
 
     def __call__(self, store, lo, hi):
         import torch
 
+        src = store.view()[lo:hi]
+        if self.dense is not None and not src.is_contiguous():
+            src = kernels.copy_rows(self.dense[lo:hi], src)
         ev = torch.cuda.Event()
         ev.record()
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(ev)
-            self.host[lo:hi].copy_(store.view()[lo:hi], non_blocking=True)
+            self.host[lo:hi].copy_(src, non_blocking=True)
 
     def finish(self):
         self.stream.synchronize()

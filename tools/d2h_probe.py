@@ -53,13 +53,29 @@ def main():
                             view[cuts[i]:cuts[i + 1]].copy_(host[cuts[i]:cuts[i + 1]],
                                                             non_blocking=True)
 
+                def d2h_2d():
+                    import ctypes
+
+                    from paper_2211_15082_b200 import _lib
+                    for i in range(chunks):
+                        st = s2 if (two and i % 2) else s1
+                        r0, r1 = cuts[i], cuts[i + 1]
+                        _lib.call("glint_copy_rows_async", host[r0].data_ptr(), dim * 4,
+                                  dev[r0].data_ptr(), pitch * 4, dim * 4, r1 - r0,
+                                  ctypes.c_void_p(st.cuda_stream))
+
                 d2h()
                 h2d()
+                d2h_2d()
+                ms_2d = min(timed(d2h_2d, (s1, s2)) for _ in range(3))
+                assert torch.equal(host, view.cpu())
                 ms_d = min(timed(d2h, (s1, s2)) for _ in range(3))
                 ms_h = min(timed(h2d, (s1, s2)) for _ in range(3))
                 print(json.dumps({"dim": dim, "pitch": pitch, "bytes": nbytes, "chunks": chunks,
                                   "two_streams": two, "d2h_ms": ms_d,
-                                  "d2h_GBps": nbytes / ms_d / 1e6, "h2d_ms": ms_h,
+                                  "d2h_GBps": nbytes / ms_d / 1e6,
+                                  "d2h_2d_ms": ms_2d, "d2h_2d_GBps": nbytes / ms_2d / 1e6,
+                                  "h2d_ms": ms_h,
                                   "h2d_GBps": nbytes / ms_h / 1e6}), flush=True)
         del dev, host
 

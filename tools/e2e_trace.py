@@ -2,6 +2,7 @@
 """Device/host timeline of one end-to-end run_inference call (host buffers)."""
 
 import json
+import os
 import pathlib
 import sys
 
@@ -30,7 +31,7 @@ def main():
     hg = CscGraph(n, g.num_edges, ip.numpy(), ix.numpy())
     del g, xt
     budget = DeviceBudget(160 << 30)
-    for rep in range(3):
+    for rep in range(int(os.environ.get("GLINT_TRACE_REPS", "3"))):
         res = None
         torch.cuda.synchronize()
         probe = KernelProbe()
