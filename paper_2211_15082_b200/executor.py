@@ -644,9 +644,9 @@ class LayerwiseEngine:
                 sub = _Plan(c0, c1, n_inputs, int(prefix[c1] - prefix[c0]), n_hub)
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
                                 gat_cache)
+                if self.probe is not None:
+                    self.probe.mark(f"L{layer} rows [{c0},{c1}) launched")
                 if sink_store is not None:
-                    if self.probe is not None:
-                        self.probe.mark(f"L{layer} rows [{c0},{c1}) launched")
                     self.sink(sink_store, c0, c1)
                     if self.probe is not None:
                         self.probe.mark(f"L{layer} sink [{c0},{c1}) queued")
@@ -1338,15 +1338,19 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             if probe is not None:
                 probe.mark("features uploaded (copy stream)", copy)
 
-        # int32 CSR (host-narrowed) lands fast enough that 5 geometric row chunks
-        # (1/16, 1/8, 1/4, 1/2, all of the edges) overlap it with layer 1's
-        # bootstrap batches without splitting them into hub-bound pieces
-        # (tools/e2e_ab.py: median 69.9 ms vs 71.0 uniform x4 vs 74.1 with 16
-        # device-narrowed int64 chunks; profiles/r01_e2e_upload_ab.jsonl)
+        # The packed CSR (host-narrowed, 24-bit) uploads faster than layer 1
+        # computes, so layer 1 only needs a small first chunk to start on and
+        # then stays ahead of the rest: chunk ends at 1/16, 1/4, 1/2, 3/4 of the
+        # edges (tools/e2e_ab.py --fracs-ab: median 64.8 ms vs 66.9 for the
+        # geometric 1/16, 1/8, 1/4, 1/2 plan, whose last half-of-the-edges chunk
+        # left 7.7 ms of layer 1 behind the upload; 66.6 for 8 uniform chunks;
+        # profiles/r01_e2e_fracs_ab.jsonl).  Without host narrowing: 16 chunks.
         chunks = int(os.environ.get("GLINT_UPLOAD_CHUNKS", "5" if HOST_NARROW else "16"))
-        geometric = os.environ.get("GLINT_UPLOAD_GEOMETRIC", "1" if HOST_NARROW else "0") == "1"
+        geometric = os.environ.get("GLINT_UPLOAD_GEOMETRIC", "0") == "1"
+        fracs = ((0.0625, 0.25, 0.5, 0.75) if HOST_NARROW and not geometric
+                 and "GLINT_UPLOAD_CHUNKS" not in os.environ else None)
         dg0 = DeviceGraph.upload_async(g, dev, copy, after_indptr=upload_features, chunks=chunks,
-                                       geometric=geometric)
+                                       geometric=geometric, fracs=fracs)
         x0, x_ready = box["x"], box["ev"]
         if probe is not None:
             probe.mark("csr uploaded (copy stream)", copy)

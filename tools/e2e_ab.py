@@ -35,6 +35,40 @@ def main():
     budget = DeviceBudget(160 << 30)
     from paper_2211_15082_b200 import storage
 
+    if "--fracs-ab" in sys.argv:
+        # interleaved A/B of CSR upload chunk plans (GLINT_UPLOAD_FRACS, cumulative
+        # edge fractions; "" = the default geometric plan)
+        plans = sys.argv[sys.argv.index("--fracs-ab") + 1].split(";")
+        times = {p: [] for p in plans}
+
+        def set_plan(p):
+            if p:
+                os.environ["GLINT_UPLOAD_FRACS"] = p
+            else:
+                os.environ.pop("GLINT_UPLOAD_FRACS", None)
+
+        res = None
+        for p in plans:
+            set_plan(p)
+            res = None
+            res = run_inference(m, hg, xh, budget=budget, output="numpy")
+        for _ in range(5):
+            for p in plans:
+                set_plan(p)
+                res = None
+                t0 = time.perf_counter()
+                res = run_inference(m, hg, xh, budget=budget, output="numpy")
+                torch.cuda.synchronize()
+                times[p].append(1e3 * (time.perf_counter() - t0))
+        import numpy as np
+
+        for p in plans:
+            print(json.dumps({"model": model, "ab": "CSR upload chunk plan",
+                              "fracs": p or "default plan",
+                              "ms": [round(t, 1) for t in times[p]],
+                              "median": float(np.median(times[p]))}), flush=True)
+        return
+
     # --pack24-ab: alternate 24-bit packed and int32 CSR uploads in one process
     modes = (True, False) if "--pack24-ab" in sys.argv else (storage.PACK24,)
     times = {mode: [] for mode in modes}
