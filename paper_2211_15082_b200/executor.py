@@ -627,8 +627,13 @@ class LayerwiseEngine:
             # CSR rows have arrived.
             cuts = {r0, r1}
             if sink_store is not None and r1 - r0 >= 2 * self.sink_chunks:
-                cuts.update(int(c) for c in np.linspace(r0, r1, self.sink_chunks + 1)
-                            .astype(np.int64))
+                env = os.environ.get("GLINT_SINK_FRACS")     # A/B: cumulative row fractions
+                if env:
+                    fr = np.asarray([float(f) for f in env.split(",")])
+                    cuts.update(int(c) for c in (r0 + fr * (r1 - r0)).astype(np.int64))
+                else:
+                    cuts.update(int(c) for c in np.linspace(r0, r1, self.sink_chunks + 1)
+                                .astype(np.int64))
             if full and gl.upload_in_flight():
                 cuts.update(h for h, _ in gl._pending if r0 < h < r1)
             cuts = sorted(cuts)

@@ -35,6 +35,11 @@ def main():
     budget = DeviceBudget(160 << 30)
     from paper_2211_15082_b200 import storage
 
+    if "--sink-ab" in sys.argv:     # same, for the output sink's row chunks
+        sys.argv[sys.argv.index("--sink-ab")] = "--fracs-ab"
+        var = "GLINT_SINK_FRACS"
+    else:
+        var = "GLINT_UPLOAD_FRACS"
     if "--fracs-ab" in sys.argv:
         # interleaved A/B of CSR upload chunk plans (GLINT_UPLOAD_FRACS, cumulative
         # edge fractions; "" = the default geometric plan)
@@ -43,9 +48,9 @@ def main():
 
         def set_plan(p):
             if p:
-                os.environ["GLINT_UPLOAD_FRACS"] = p
+                os.environ[var] = p
             else:
-                os.environ.pop("GLINT_UPLOAD_FRACS", None)
+                os.environ.pop(var, None)
 
         res = None
         for p in plans:
@@ -63,7 +68,7 @@ def main():
         import numpy as np
 
         for p in plans:
-            print(json.dumps({"model": model, "ab": "CSR upload chunk plan",
+            print(json.dumps({"model": model, "ab": f"chunk plan ({var})",
                               "fracs": p or "default plan",
                               "ms": [round(t, 1) for t in times[p]],
                               "median": float(np.median(times[p]))}), flush=True)
