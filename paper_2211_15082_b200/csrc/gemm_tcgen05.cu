@@ -513,10 +513,17 @@ int launch_bn(const TcArgs& a, int act, cudaStream_t s) {
 #ifndef GLINT_GEMM_RA1
 #define GLINT_GEMM_RA1 8
 #endif
+#ifndef GLINT_GEMM_RL1
+#define GLINT_GEMM_RL1 2
+#endif
+#ifndef GLINT_GEMM_RL2
+#define GLINT_GEMM_RL2 2
+#endif
+#ifndef GLINT_GEMM_RW1
+#define GLINT_GEMM_RW1 3
+#endif
 namespace v2 {
 
-constexpr int RL = 2;   // A "lo" ring (computed by the producers)
-constexpr int RW = 3;   // W panel ring (TMA bulk copies)
 constexpr int kEpiWarps2 = 8;
 constexpr int kScMaxN = 512;               // widest Z row with the fused score epilogue
 
@@ -540,6 +547,11 @@ struct Cfg2 {
   // raw-A ring (cp.async, also the TF32 "hi" operand): 128-row tiles have the
   // shared memory for a deeper ring (more loads in flight per SM)
   static constexpr int RA = MH == 1 ? GLINT_GEMM_RA1 : 6;
+  // A "lo" ring (computed by the producers): the producer of lo(k) waits for
+  // the MMAs of k - RL to retire, so RL bounds how far lo runs ahead of the
+  // tensor pipe; W panel ring (TMA bulk copies from L2)
+  static constexpr int RL = MH == 1 ? GLINT_GEMM_RL1 : (BN <= 96 ? GLINT_GEMM_RL2 : 2);
+  static constexpr int RW = MH == 1 ? GLINT_GEMM_RW1 : 3;
   static constexpr int A_BYTES = TM * BK * 4;  // one raw / lo slot (TM x 16 fp32)
   static constexpr int W_BYTES = BN * BK * 4;  // one of W hi / lo
   static constexpr int RAW_OFF = 0;
@@ -696,8 +708,8 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
   constexpr int PER = C::TM * 4 / Rl::PT;   // 16-byte chunks per producer thread
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_empty[C::RA];
-  __shared__ __align__(8) uint64_t lo_full[RL], lo_empty[RL];
-  __shared__ __align__(8) uint64_t w_full[RW], w_empty[RW];
+  __shared__ __align__(8) uint64_t lo_full[C::RL], lo_empty[C::RL];
+  __shared__ __align__(8) uint64_t w_full[C::RW], w_empty[C::RW];
   __shared__ __align__(8) uint64_t tmem_full[2];
   __shared__ __align__(8) uint64_t tmem_empty[2];
   __shared__ uint32_t tmem_slot;
@@ -712,11 +724,11 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::RA; ++i) mbar_init(&raw_empty[i], 1);           // tcgen05.commit
-    for (int i = 0; i < RL; ++i) {
+    for (int i = 0; i < C::RL; ++i) {
       mbar_init(&lo_full[i], Rl::PW);                           // one per producer warp
       mbar_init(&lo_empty[i], 1);
     }
-    for (int i = 0; i < RW; ++i) {
+    for (int i = 0; i < C::RW; ++i) {
       mbar_init(&w_full[i], 1);                                         // expect_tx arrive
       mbar_init(&w_empty[i], 1);
     }
@@ -778,8 +790,8 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
     for (int64_t idx = 0; idx < total; ++idx) {
       asm volatile("cp.async.wait_group %0;" ::"n"(C::RA - 2) : "memory");  // own copies of idx landed
       const int rs = static_cast<int>(idx % C::RA);
-      const int ls = static_cast<int>(idx % RL);
-      const uint32_t luse = static_cast<uint32_t>(idx / RL);
+      const int ls = static_cast<int>(idx % C::RL);
+      const uint32_t luse = static_cast<uint32_t>(idx / C::RL);
       mbar_wait(&lo_empty[ls], (luse & 1u) ^ 1u);
       const uint8_t* raw = smem + C::RAW_OFF + rs * C::A_BYTES;
       uint8_t* lo = smem + C::LO_OFF + ls * C::A_BYTES;
@@ -807,8 +819,8 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
         const int64_t tile = blockIdx.x + (idx / nkb) * gridDim.x;
         const int nt = static_cast<int>(tile % a.n_tiles);
         const int kb = static_cast<int>(idx % nkb);
-        const int s = static_cast<int>(idx % RW);
-        const uint32_t use = static_cast<uint32_t>(idx / RW);
+        const int s = static_cast<int>(idx % C::RW);
+        const uint32_t use = static_cast<uint32_t>(idx / C::RW);
         mbar_wait(&w_empty[s], (use & 1u) ^ 1u);
         mbar_arrive_expect_tx(&w_full[s], 2 * C::W_BYTES);
         bulk_g2s(smem + C::W_OFF + s * 2 * C::W_BYTES,
@@ -827,11 +839,11 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
       for (int kb = 0; kb < nkb; ++kb) {
         const int64_t idx = it * nkb + kb;
         const int rs = static_cast<int>(idx % C::RA);
-        const int ls = static_cast<int>(idx % RL);
-        const int ws = static_cast<int>(idx % RW);
+        const int ls = static_cast<int>(idx % C::RL);
+        const int ws = static_cast<int>(idx % C::RW);
         if (!a.mma_only) {   // a.mma_only: diagnostics, MMA issue rate without operand waits
-          mbar_wait(&lo_full[ls], static_cast<uint32_t>(idx / RL) & 1u);
-          mbar_wait(&w_full[ws], static_cast<uint32_t>(idx / RW) & 1u);
+          mbar_wait(&lo_full[ls], static_cast<uint32_t>(idx / C::RL) & 1u);
+          mbar_wait(&w_full[ws], static_cast<uint32_t>(idx / C::RW) & 1u);
         }
         fence_after();
         if (lane == 0) {
