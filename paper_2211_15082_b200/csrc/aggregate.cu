@@ -500,7 +500,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int LPR, int VPL, int R, int STRIDE = kThreads, int B = 1>
+// base + u * ld_bytes as ONE 32x32->64 multiply-add (IMAD.WIDE): the hot
+// loops' source-row address (row ids < 2^31, row pitch < 2^31 bytes).
+__device__ __forceinline__ const float* row_at(const char* base, int32_t u, int32_t ld_bytes) {
+  const char* p;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(u), "r"(ld_bytes), "l"(base));
+  return reinterpret_cast<const float*>(p);
+}
+
+// MAP = false: no column map (full mode), so the per-edge id needs no lookup.
+template <int LPR, int VPL, int R, int STRIDE = kThreads, int B = 1, bool MAP = true>
 __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int lane_g,
                                                unsigned gmask, float4* ring, int col0 = 0) {
   // ring: this lane's slots, slot (t, k) at ring[(t * VPL + k) * STRIDE]; the
@@ -515,8 +524,8 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   for (int k = 0; k < VPL; ++k) ok[k] = col0 + (lane_g + LPR * k) * 4 < a.dim;
   const uint32_t ring_s = smem_u32(ring);
 
-  const float* hbase = a.h + col0 + lane_g * 4;
-  const int32_t ld32 = static_cast<int32_t>(a.ld_h);
+  const char* hbase = reinterpret_cast<const char*>(a.h + col0 + lane_g * 4);
+  const int32_t ldb = static_cast<int32_t>(a.ld_h * 4);
   // issue cursor: edge `ie`, index chunk [cb, cb+LPR) held in `cur`, next in `nxt`
   int ie = 0, cb = 0;
   int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
@@ -527,8 +536,8 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
       cur = nxt;
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
     }
-    const int32_t u = a.ra.map32(__shfl_sync(gmask, cur, ie - cb, LPR));
-    const float* src = hbase + static_cast<int64_t>(u) * ld32;   // one IMAD.WIDE
+    const int32_t id = __shfl_sync(gmask, cur, ie - cb, LPR);
+    const float* src = row_at(hbase, MAP ? a.ra.map32(id) : id, ldb);
 #pragma unroll
     for (int k = 0; k < VPL; ++k)
       if (ok[k])
@@ -599,7 +608,7 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   }
 }
 
-template <int LPR, int VPL, int R, int MINB, int B = 1>
+template <int LPR, int VPL, int R, int MINB, int B = 1, bool MAP = true>
 __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) {
   extern __shared__ __align__(16) float4 ring_all[];
   constexpr int G = 32 / LPR;
@@ -612,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) 
   if (idx >= a.sc.n_rows) return;
   const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
   const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
-  mean_row_async<LPR, VPL, R, kThreads, B>(a, r, lane_g, gmask, ring_all + threadIdx.x);
+  mean_row_async<LPR, VPL, R, kThreads, B, MAP>(a, r, lane_g, gmask, ring_all + threadIdx.x);
 }
 
 // Hub rows, per-lane cp.async ring: one warp per (hub row, 128-column block),
@@ -656,7 +665,9 @@ int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
   constexpr int smem = R * VPL * kThreads * 16;
   static bool configured = false;
   if (!configured) {
-    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B>,
+    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
@@ -666,7 +677,10 @@ int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
     set_error("spmm_mean: grid too large");
     return GLINT_EINVAL;
   }
-  mean_async_kernel<LPR, VPL, R, MINB, B><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  if (a.ra.col_map)
+    mean_async_kernel<LPR, VPL, R, MINB, B, true><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  else
+    mean_async_kernel<LPR, VPL, R, MINB, B, false><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   return launch_status("spmm_mean_async");
 }
 
@@ -1872,7 +1886,7 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
   GLINT_REQUIRE(dim > 0, "spmm_mean: dim must be > 0");
   GLINT_REQUIRE(indptr && h && out, "spmm_mean: null indptr/h/out");
   GLINT_REQUIRE(ld_h >= dim && ld_out >= dim, "spmm_mean: leading dimension < dim");
-  GLINT_REQUIRE(ld_h < (1LL << 31), "spmm_mean: ld_h must be < 2^31");
+  GLINT_REQUIRE(ld_h < (1LL << 29), "spmm_mean: ld_h must be < 2^29 (row pitch in bytes < 2^31)");
   GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows, "spmm_mean: n_hub out of range");
   GLINT_REQUIRE(schedule || n_hub == 0, "spmm_mean: hub rows need a schedule");
   GLINT_REQUIRE(act >= GLINT_ACT_NONE && act <= GLINT_ACT_LEAKY_RELU, "spmm_mean: bad act %d", act);
