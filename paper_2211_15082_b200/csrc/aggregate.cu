@@ -1207,6 +1207,8 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   }
 
   const uint32_t zr = smem_u32(zring);
+  const char* zbase = reinterpret_cast<const char*>(a.Z + lane_g * 4);
+  const int32_t ldzb = static_cast<int32_t>(a.ldz * 4);
   int ie = 0, cb = 0;
   int32_t ucur = (lane_g < deg) ? a.ra.map32(__ldg(a.ra.indices + beg + lane_g)) : 0;
   int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
@@ -1219,9 +1221,7 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
       if (cb + lane_g < deg) sc = load_scores<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec);
     }
-    const int64_t off = static_cast<int64_t>(__shfl_sync(gmask, ucur, ie - cb, LPR)) *
-                        static_cast<int32_t>(a.ldz);
-    const float* zsrc = a.Z + off + lane_g * 4;
+    const float* zsrc = row_at(zbase, __shfl_sync(gmask, ucur, ie - cb, LPR), ldzb);
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
@@ -1964,7 +1964,7 @@ int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim, 
   GLINT_REQUIRE(heads >= 1 && heads <= kMaxHeads, "gat_aggregate: heads must be in [1, %d]", kMaxHeads);
   GLINT_REQUIRE(head_dim >= 1 && head_pitch >= head_dim && head_pitch % 4 == 0,
                 "gat_aggregate: head_pitch must be a multiple of 4 and >= head_dim");
-  GLINT_REQUIRE(ldz < (1LL << 31), "gat_aggregate: ldz must be < 2^31");
+  GLINT_REQUIRE(ldz < (1LL << 29), "gat_aggregate: ldz must be < 2^29 (row pitch in bytes < 2^31)");
   GLINT_REQUIRE(ldz % 4 == 0 && ldz >= static_cast<int64_t>(heads) * head_pitch && aligned16(Z),
                 "gat_aggregate: Z must be 16B aligned with ldz %% 4 == 0 and ldz >= heads*head_pitch");
   GLINT_REQUIRE(indptr && Z && s_src && s_dst && out, "gat_aggregate: null argument");
