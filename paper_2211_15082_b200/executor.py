@@ -636,6 +636,8 @@ class LayerwiseEngine:
                                 .astype(np.int64))
             if full and gl.upload_in_flight():
                 cuts.update(h for h, _ in gl._pending if r0 < h < r1)
+            if full and self.exchange is not None and hasattr(self.exchange, "piece_bounds"):
+                cuts.update(b for b in self.exchange.piece_bounds() if r0 < b < r1)
             cuts = sorted(cuts)
             if hub_host is not None:
                 hubs = hub_host[np.asarray(cuts)]

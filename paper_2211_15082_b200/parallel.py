@@ -94,6 +94,12 @@ class RowExchange:
                                                       async_op=True))
             self._posted += 1
 
+    def piece_bounds(self):
+        """Row bounds of this rank's pieces: the engine cuts its launches there,
+        so each finished piece is broadcast while the next one computes (one
+        whole-layer launch would leave nothing to overlap)."""
+        return [self._piece(self.rank, c)[1] for c in range(self.chunks)]
+
     def progress(self, engine, blk, done_hi):
         """Rows [.., done_hi) of this rank's range are computed for `blk`."""
         if self._blk is not blk:

@@ -143,3 +143,15 @@ def test_row_exchange_overlapped_pieces_gloo(world):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in results)
     assert sum(b for _, _, b in results) == 41 * 3 * 4
+
+
+def test_piece_bounds_cut_the_rank_range():
+    """The engine cuts its launches at piece_bounds(), so each piece can be
+    broadcast while the next computes; the bounds tile this rank's range."""
+    from paper_2211_15082_b200.parallel import RowExchange
+
+    ex = RowExchange(np.array([0, 10, 25]), rank=1, world=2, chunks=4)
+    assert ex.piece_bounds() == [13, 17, 21, 25]
+    assert [ex._piece(1, c) for c in range(4)] == [(10, 13), (13, 17), (17, 21), (21, 25)]
+    ex0 = RowExchange(np.array([0, 10, 25]), rank=0, world=2, chunks=3)
+    assert ex0.piece_bounds() == [3, 6, 10]
