@@ -46,8 +46,14 @@ def main():
     ap.add_argument("--variants", type=int, default=5)
     ap.add_argument("--gemm", default="100x256,256x256,256x47,256x192,100x192")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--tune", action="append", default=[],
+                    help="glint_set_tuning KEY=VALUE applied before the sweep")
     args = ap.parse_args()
     args.what = set(args.what.split(","))
+    for kv in args.tune:
+        k, v = kv.split("=")
+        _lib.call("glint_set_tuning", int(k), int(v))
+        print(json.dumps({"tuning": {int(k): int(v)}}), flush=True)
     n = args.nodes
     und = int(round(n * synth.PRODUCTS_UNDIRECTED / synth.PRODUCTS_NODES))
     g = synth.gen_products_like(n, und, seed=0, device="cuda") \
