@@ -1247,15 +1247,16 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   int slot = 0, jc = 0;
   for (int j = 0; j < deg; ++j) {
     if (jc == 0) {   // consumption enters a chunk: its weights from the staged scores
+      __syncwarp(gmask);   // every lane is done with the previous chunk's weights
       if (j + lane_g < deg) {
 #pragma unroll
         for (int h = 0; h < H; ++h)
           wbuf[lane_g * H + h] =
               expf(__fsub_rn(leaky(__fadd_rn(sc.v[h], sdst[h]), a.slope), peak[h]));
       }
+      __syncwarp(gmask);   // the chunk's weights are visible
     }
-    cp_async_wait<R - 1>();
-    __syncwarp(gmask);   // ring slot landed; the chunk's weights are visible
+    cp_async_wait<R - 1>();   // this lane's ring slot landed (slots are per lane)
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
@@ -1268,7 +1269,6 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
         num[k][3] = __fadd_rn(num[k][3], __fmul_rn(w, v.w));
       }
     }
-    __syncwarp(gmask);   // every lane is done with the slot (and the chunk) before refills
     if (ie < deg) issue(slot);
     cp_async_commit();
     slot = (slot + 1 == R) ? 0 : slot + 1;
