@@ -539,3 +539,25 @@ def test_packed_upload_rejects_wide_ids(cuda):
             assert rc == 0 and dst.cpu().tolist() == ids
         else:
             assert rc != 0 and "24 bits" in _lib.last_error()
+
+
+def test_async_upload_wide_ids_use_int32(cuda):
+    """N > 2^24: ids no longer fit 24 bits, so the upload narrows to int32 (the
+    packed path is only taken when every id fits); ids near 2^24 and N-1 land
+    intact."""
+    import torch
+
+    from paper_2211_15082_b200 import storage
+
+    n = (1 << 24) + 5
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    ids = np.array([0, (1 << 24) - 1, 1 << 24, (1 << 24) + 1, n - 1, 12345], dtype=np.int64)
+    ptr[3:] = 2                     # node 2 gets ids[0:2]
+    ptr[n - 1:] = 6                 # node n-2 gets ids[2:6]
+    ptr[-1] = 6
+    g = storage.CscGraph(n, 6, ptr, ids)
+    copy = torch.cuda.Stream()
+    dg = storage.DeviceGraph.upload_async(g, torch.device("cuda"), copy, chunks=2)
+    dg.wait_rows()
+    torch.cuda.synchronize()
+    assert dg.indices.cpu().numpy().tolist() == ids.tolist()
