@@ -1394,10 +1394,11 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             eng.sink = streamed
             if "GLINT_SINK_CHUNKS" not in os.environ:
                 # the device->host copy outlasts the last layer, so it should
-                # start early: ~128 MiB chunks, 4..16 of them (tools/e2e_ab.py:
-                # GCN 4 chunks 69.0 vs 69.6 ms with 2; GAT 16 chunks 121.6 vs 130)
+                # start early: ~128 MiB chunks, 8..16 of them (tools/e2e_ab.py
+                # --sink-ab: GCN 8 uniform chunks 63.6 ms vs 64.4 with 4;
+                # profiles/r01_e2e_sink_ab.jsonl)
                 out_bytes = g.num_nodes * m.output_dim * 4
-                eng.sink_chunks = int(min(16, max(4, round(out_bytes / (128 << 20)))))
+                eng.sink_chunks = int(min(16, max(8, round(out_bytes / (128 << 20)))))
         eng.probe = probe
         store = eng.run(exchange=ex)
         if ex is not None:
