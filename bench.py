@@ -407,7 +407,7 @@ def main():
     del x
     if rank == 0 and world == 1 and not args.no_cpu:
         indptr, indices = host_csc(g)
-        sample = args.cpu_sample or 8192
+        sample = args.cpu_sample or 32768      # ~10 s of single-core CPU work
         rate, secs, sdesc = cpu_sample_rate(indptr, indices, m, sample)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                                 "sample": sdesc, "seconds": secs,
