@@ -1576,7 +1576,22 @@ __global__ void __launch_bounds__((CW + 1) * 32) gat_hub_ring_kernel(GatArgs a, 
         pk[h] = leaky(__fadd_rn(__ldg(a.s_src + self * H + h), sd[h]), a.slope);
       }
     }
-    for (int64_t e = beg + tid; e < end; e += (CW * 32)) {
+    // four independent index -> score chains in flight per thread (a hub row
+    // has up to ~2e4 edges: one dependent pair per step would bound the pass)
+    constexpr int kStride = CW * 32;
+    int64_t e = beg + tid;
+    for (; e + 3 * kStride < end; e += 4 * kStride) {
+      int64_t u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = a.ra.map(__ldg(a.ra.indices + e + q * kStride));
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h)
+          if (h < H)
+            pk[h] = fmaxf(pk[h], leaky(__fadd_rn(__ldg(a.s_src + u[q] * H + h), sd[h]), a.slope));
+    }
+    for (; e < end; e += kStride) {
       const int64_t u = a.ra.map(a.ra.indices[e]);
 #pragma unroll
       for (int h = 0; h < kMaxHeads; ++h)
@@ -1612,7 +1627,18 @@ __global__ void __launch_bounds__((CW + 1) * 32) gat_hub_ring_kernel(GatArgs a, 
       consumer_sync<CW>();
       const int64_t e0 = beg + wbase;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kGatWChunk), end - e0));
-      for (int t = tid; t < cnt; t += (CW * 32)) {
+      int t = tid;
+      for (; t + 3 * (CW * 32) < cnt; t += 4 * (CW * 32)) {   // 4 chains in flight
+        int64_t u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = a.ra.map(__ldg(a.ra.indices + e0 + t + q * (CW * 32)));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          for (int h = 0; h < H; ++h)
+            w_sm[(t + q * (CW * 32)) * H + h] = expf(__fsub_rn(
+                leaky(__fadd_rn(__ldg(a.s_src + u[q] * H + h), s_sd[h]), a.slope), s_pk[h]));
+      }
+      for (; t < cnt; t += (CW * 32)) {
         const int64_t u = a.ra.map(a.ra.indices[e0 + t]);
         for (int h = 0; h < H; ++h)
           w_sm[t * H + h] = expf(
