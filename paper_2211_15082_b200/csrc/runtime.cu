@@ -75,19 +75,22 @@ int glint_abi_version(void) { return 1; }
 
 int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                       size_t* free_bytes, size_t* total_bytes) {
+  // cudaDeviceGetAttribute, not cudaGetDeviceProperties: the latter costs
+  // milliseconds to tens of ms per call (it gathers every property), and the
+  // request path asks for free HBM once per run_inference (budget="device").
   int prev = 0;
   GLINT_CUDA(cudaGetDevice(&prev));
-  GLINT_CUDA(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  GLINT_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (sm_count) *sm_count = prop.multiProcessorCount;
-  if (cc_major) *cc_major = prop.major;
-  if (cc_minor) *cc_minor = prop.minor;
-  size_t f = 0, t = 0;
-  GLINT_CUDA(cudaMemGetInfo(&f, &t));
-  if (free_bytes) *free_bytes = f;
-  if (total_bytes) *total_bytes = t;
-  GLINT_CUDA(cudaSetDevice(prev));
+  if (prev != device) GLINT_CUDA(cudaSetDevice(device));
+  if (sm_count) GLINT_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  if (cc_major) GLINT_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  if (cc_minor) GLINT_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (free_bytes || total_bytes) {
+    size_t f = 0, t = 0;
+    GLINT_CUDA(cudaMemGetInfo(&f, &t));
+    if (free_bytes) *free_bytes = f;
+    if (total_bytes) *total_bytes = t;
+  }
+  if (prev != device) GLINT_CUDA(cudaSetDevice(prev));
   return GLINT_OK;
 }
 

@@ -322,12 +322,22 @@ _PARAM_CACHE: dict = {}
 
 
 def _plan_stream(device):
-    """One planning side stream per device, reused by every engine."""
+    """One planning side stream per device, reused by every engine.
+
+    High priority: the controller's n_inputs counts are a chain of host
+    round trips (each plan depends on the previous batch's adapt step), issued
+    while a whole-layer aggregation fills the GPU.  At default priority their
+    small kernels queued behind every pending aggregation CTA, so the chain
+    ran only after the layer finished and left the device idle ~1.6 ms per
+    step between layers 1 and 2 (tools/order_timeline.py); at high priority
+    the block scheduler slots them in as aggregation CTAs retire.
+    GLINT_PLAN_PRIORITY=0 restores the default (A/B)."""
     import torch
 
     s = _PLAN_STREAMS.get(device)
     if s is None:
-        s = _PLAN_STREAMS[device] = torch.cuda.Stream(device=device)
+        prio = -1 if os.environ.get("GLINT_PLAN_PRIORITY", "1") == "1" else 0
+        s = _PLAN_STREAMS[device] = torch.cuda.Stream(device=device, priority=prio)
     return s
 
 
@@ -373,11 +383,15 @@ class LayerwiseEngine:
 
     def __init__(self, m: ModelGraph, schedule: BlockSchedule, g: DeviceGraph, x: DeviceStore,
                  tsets: TargetSets, budget, thresholds: Thresholds, stats: RunStats,
-                 precision=None, row_range=None, reassociate=True, release_input=False):
+                 precision=None, row_range=None, reassociate=False, release_input=False):
         import torch
 
         self.m, self.schedule, self.g, self.tsets = m, schedule, g, tsets
+        # opt-in: mean(h)W^T+b vs mean(hW^T)+b differ at ~1e-7 in fp32, so the
+        # reference contract (layer-wise == node-wise == eval_reference bytes)
+        # holds only with reassociation off, the default
         self.reassociate = reassociate
+        self.retain_stores = False          # checkers: keep every layer's store alive
         self.release_input = release_input  # engine owns x: free it after its last reader
         self.budget, self.stats = budget, stats
         self.controller = BatchController(thresholds=thresholds, budget=budget)
@@ -912,6 +926,8 @@ class LayerwiseEngine:
         return sched
 
     def release_after(self, blk):
+        if self.retain_stores:
+            return
         out_key = self.schedule.model_output.key
         keep = (out_key,) if self.release_input else (INPUT_REF, out_key)
         for key, last in self.schedule.drop_after.items():
@@ -1287,7 +1303,7 @@ def _exchange_for(distributed, mode, g):
 def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanout=None, seed=0,
                   executor="layerwise", order="none", budget=None, thresholds=None,
                   batch_size=1024, store_backing="memory", workdir=None, output="auto",
-                  precision=None, distributed="auto", reassociate=True,
+                  precision=None, distributed="auto", reassociate=False,
                   probe=None) -> InferenceResult:
     """End to end: reorder, annotate, execute, de-permute (glint/executor.py:481-543).
 
@@ -1300,6 +1316,11 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     an initialised torch.distributed group (one process per GPU, NCCL); each
     rank computes its edge-balanced node range and returns the full output.
     Batch records / stats then describe the calling rank's own batches.
+    ``reassociate=True`` (opt-in) computes a width-narrowing ConvMean as
+    mean(h W^T) + b: exact in real arithmetic, ~1e-7 apart in fp32, and it
+    gathers d_out instead of d_in floats per edge.  Off by default so that
+    layer-wise, node-wise and eval_reference stay byte-identical, as in the
+    reference (glint/executor.py:481-543).
     """
     import torch
 

@@ -69,7 +69,8 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.reset_peak_memory_stats()
         stats = RunStats("layerwise", "full", "none", m.depth, (th0.n_t, th0.n_i))
-        eng = LayerwiseEngine(m, schedule, g, x, tsets, budget, th0, stats, release_input=True)
+        eng = LayerwiseEngine(m, schedule, g, x, tsets, budget, th0, stats, release_input=True,
+                              reassociate=True)
         del x
         probe = KernelProbe()
         eng.probe = probe

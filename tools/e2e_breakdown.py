@@ -57,14 +57,14 @@ def main():
         sched = split(m)
         ts = annotate(dg, np.arange(n), 3, "full")
         st = RunStats("layerwise", "full", "none", 3)
-        eng = LayerwiseEngine(m, sched, dg, x, ts, budget, Thresholds(1024, 32768), st)
+        eng = LayerwiseEngine(m, sched, dg, x, ts, budget, Thresholds(1024, 32768), st, reassociate=True)
         store = eng.run()
         t = tick("engine_ms", t)
         host = torch.empty((n, 47), dtype=torch.float32, pin_memory=True)
         host.copy_(store.view())
         t = tick("output_d2h_ms", t)
         t0 = time.perf_counter()
-        res = run_inference(m, hg, xh, budget=budget, output="numpy")
+        res = run_inference(m, hg, xh, budget=budget, output="numpy", reassociate=True)
         torch.cuda.synchronize()
         out["run_inference_ms"] = (time.perf_counter() - t0) * 1e3
         del res, dg, x, store, eng
@@ -74,7 +74,7 @@ def main():
 
     pr = cProfile.Profile()
     pr.enable()
-    res = run_inference(m, hg, xh, budget=budget, output="numpy")
+    res = run_inference(m, hg, xh, budget=budget, output="numpy", reassociate=True)
     torch.cuda.synchronize()
     pr.disable()
     pstats.Stats(pr).sort_stats("tottime").print_stats(25)

@@ -35,7 +35,7 @@ def main():
         res = None
         torch.cuda.synchronize()
         probe = KernelProbe()
-        res = run_inference(m, hg, xh, budget=budget, output="numpy", probe=probe)
+        res = run_inference(m, hg, xh, budget=budget, output="numpy", probe=probe, reassociate=True)
         torch.cuda.synchronize()
         probe.mark("end")
         torch.cuda.synchronize()
