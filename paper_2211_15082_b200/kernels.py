@@ -539,7 +539,7 @@ def linear_into(C, x, w, bias, act, a_rows=None, precision=None):
 
 def linear(x, weight, bias=None):
     """out[i] = weight @ x[i] (+ bias) (glint/kernels.py:95-107)."""
-    host = _is_host(x, weight, bias)
+    host = _is_host(x)     # the container kind follows the data, not the parameters
     xd, wd = _f32(x), _f32(weight)
     if xd.dim() != 2 or wd.dim() != 2 or xd.shape[1] != wd.shape[1]:
         raise ValueError(f"linear shape mismatch: x {tuple(xd.shape)} vs weight {tuple(wd.shape)}")

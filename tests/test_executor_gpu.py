@@ -51,9 +51,9 @@ def test_all_golden_cases(golden, cuda):
 
 def test_nodewise_equals_layerwise_bytes(golden, cuda):
     """Both engines share kernels; batch invariance makes them bit-identical
-    (reference test_executor.py:109-180).  Compared on the aggregate-first
-    path: the layer-wise reassociation of narrowing convs is a different (but
-    equally row-invariant) fp32 evaluation order."""
+    (reference test_executor.py:109-180), with the drop-in API's default
+    settings (reassociation is opt-in: it is a different, equally
+    row-invariant, fp32 evaluation order)."""
     from test_host_logic import golden_models
 
     arrs, meta = golden
@@ -62,7 +62,7 @@ def test_nodewise_equals_layerwise_bytes(golden, cuda):
     for case in meta["e2e"]:
         if case["graph"] not in ("toy", "reg200") or case["budget"] != 1 << 30:
             continue
-        lw = _run(case, arrs, models, reassociate=False)
+        lw = _run(case, arrs, models)
         nw = _run(case, arrs, models, executor="nodewise", batch_size=7)
         assert lw.output.tobytes() == nw.output.tobytes(), case["name"]
         done += 1
@@ -241,6 +241,7 @@ def test_bench_json_contract():
     import sys
 
     root = pathlib.Path(__file__).resolve().parents[1]
+    configs = []
     for extra in ([], ["--impl", "reference"]):
         out = subprocess.run([sys.executable, str(root / "bench.py"), "--nodes", "20000",
                               "--steps", "2", "--warmup", "3", "--cpu-sample", "256"] + extra,
@@ -254,6 +255,7 @@ def test_bench_json_contract():
                   "cpu_baseline", "e2e"):
             assert k in d, k
         assert d["value"] > 0 and "workload" in d["config"]
+        configs.append((d["config"], d["metric"], d["unit"], d["data"]))
         if extra:
             assert d["impl"] == "reference" and d["e2e"]["h2d_bytes_per_step"] == 0
         else:
@@ -267,3 +269,7 @@ def test_bench_json_contract():
                 assert k in d["e2e"], k
             for k in ("value", "unit", "cores", "kind", "sample"):
                 assert k in d["cpu_baseline"], k
+            p = d["parity"]
+            assert p["pass"] and p["k1_bytes_equal"] and p["records_equal"], p
+            assert d["secondary"]["cfg3"]["parity"]["pass"]
+    assert configs[0] == configs[1]         # the driver's same_config
