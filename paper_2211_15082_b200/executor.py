@@ -628,6 +628,14 @@ class LayerwiseEngine:
         fused = self._fusions(blk)
         gat_cache = {}
         n_convs = sum(1 for _, k, _ in blk.iter_ops() if k in ("ConvMean", "ConvAttn"))
+        # Transform-first convs (reassociated ConvMean, ConvAttn) transform their
+        # source rows once per layer, before any batch, on EVERY rank: in a
+        # distributed run the exchange of the transformed rows is a collective
+        # that a rank with an empty row range must join too.
+        if blk.has_conv and (hi > lo or self.exchange is not None):
+            for o in blk.op_ids:
+                if blk.kinds[o] in ("ConvMean", "ConvAttn") and self.transform_first(o):
+                    gat_cache[o] = self._transform(o, layer_mats, layer_spaces)
 
         out_key = self.schedule.model_output.key
         sink_store = (self.stores.get(out_key) if self.sink is not None
@@ -788,24 +796,8 @@ class LayerwiseEngine:
                 # mean(h) W^T + b == mean(h W^T) + b: transform all source rows
                 # once per layer (narrower), aggregate the narrow rows with the
                 # bias + activation in the aggregation epilogue.
-                h, cmap = conv_source(op.inputs[0])
-                d_in, d_out = int(h.shape[1]), m.out_dims[o]
-                if o not in gat_cache:
-                    zfull = torch.empty((h.shape[0], pitch_of(d_out)), dtype=torch.float32,
-                                        device=self.dev)
-                    z = zfull[:, :d_out]
-                    own = self._own_source_rows(h)
-                    lo, hi = own if own else (0, int(h.shape[0]))
-                    if self.probe is not None:
-                        self.probe.begin("linear")
-                    kernels.linear_into(z[lo:hi], h[lo:hi], self.params.w[o], None, _lib.ACT_NONE,
-                                        precision=self.precision)
-                    if self.probe is not None:
-                        self.probe.end(2 * (hi - lo) * d_in * d_out)
-                    if own:     # every rank sends its transformed rows (d_out wide, not d_in)
-                        self.exchange.exchange_tensor(zfull)
-                    gat_cache[o] = z
-                    self.kernel_launches += 1
+                _h, cmap = conv_source(op.inputs[0])
+                d_out = m.out_dims[o]
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, d_out)
@@ -848,29 +840,9 @@ class LayerwiseEngine:
                 if act_op is None:
                     mats[o] = out
             elif op.kind == "ConvAttn":
-                h, cmap = conv_source(op.inputs[0])
+                _h, cmap = conv_source(op.inputs[0])
                 W = op.params["weight"]
                 H, dh = int(W.shape[0]), int(W.shape[1])
-                if o not in gat_cache:
-                    own = self._own_source_rows(h)
-                    lo, hi = own if own else (0, int(h.shape[0]))
-                    n_src = int(h.shape[0])
-                    proj = (torch.empty((n_src, H * kernels.head_pitch(dh)), dtype=torch.float32,
-                                        device=self.dev),
-                            torch.empty((n_src, H), dtype=torch.float32, device=self.dev),
-                            torch.empty((n_src, H), dtype=torch.float32, device=self.dev))
-                    if self.probe is not None:
-                        self.probe.begin("linear")
-                    kernels.attn_project(h[lo:hi], self.params.w_pad[o], self.params.attn[o], H, dh,
-                                         precision=self.precision,
-                                         out=tuple(t[lo:hi] for t in proj))
-                    if self.probe is not None:
-                        self.probe.end(2 * (hi - lo) * int(h.shape[1]) * H * kernels.head_pitch(dh))
-                    if own:     # exchange the projected rows and scores, not the source rows
-                        for t in proj:
-                            self.exchange.exchange_tensor(t)
-                    gat_cache[o] = proj
-                    self.kernel_launches += 2
                 Z, s_src, s_dst = gat_cache[o]
                 act_op = fused.get(o)
                 target = act_op or o
@@ -911,6 +883,50 @@ class LayerwiseEngine:
                 if mat.data_ptr() != view.data_ptr():
                     kernels.copy_rows(view, mat)
                     self.kernel_launches += 1
+
+    def _transform(self, o, layer_mats, layer_spaces):
+        """Per-layer source transform of a transform-first conv: z = h W^T for a
+        reassociated ConvMean; (Z, s_src, s_dst) for a ConvAttn.  In distributed
+        full mode each rank transforms its own rows and the result is exchanged."""
+        import torch
+
+        op = self.m.operators[o]
+        p = op.inputs[0]
+        h = (layer_mats[p] if p in layer_mats
+             else self.stores[_ref_key(self.schedule, self.m, p)].view())
+        own = self._own_source_rows(h)
+        lo, hi = own if own else (0, int(h.shape[0]))
+        n_src = int(h.shape[0])
+        if op.kind == "ConvMean":
+            d_in, d_out = int(h.shape[1]), self.m.out_dims[o]
+            zfull = torch.empty((n_src, pitch_of(d_out)), dtype=torch.float32, device=self.dev)
+            z = zfull[:, :d_out]
+            if self.probe is not None:
+                self.probe.begin("linear")
+            kernels.linear_into(z[lo:hi], h[lo:hi], self.params.w[o], None, _lib.ACT_NONE,
+                                precision=self.precision)
+            if self.probe is not None:
+                self.probe.end(2 * (hi - lo) * d_in * d_out)
+            if own:     # every rank sends its transformed rows (d_out wide, not d_in)
+                self.exchange.exchange_tensor(zfull)
+            self.kernel_launches += 1
+            return z
+        W = op.params["weight"]
+        H, dh = int(W.shape[0]), int(W.shape[1])
+        proj = (torch.empty((n_src, H * kernels.head_pitch(dh)), dtype=torch.float32,
+                            device=self.dev),
+                torch.empty((n_src, H), dtype=torch.float32, device=self.dev),
+                torch.empty((n_src, H), dtype=torch.float32, device=self.dev))
+        if self.probe is not None:
+            self.probe.begin("linear")
+        kernels.attn_project(h[lo:hi], self.params.w_pad[o], self.params.attn[o], H, dh,
+                             precision=self.precision, out=tuple(t[lo:hi] for t in proj))
+        if self.probe is not None:
+            self.probe.end(2 * (hi - lo) * int(h.shape[1]) * H * kernels.head_pitch(dh))
+        if own:     # exchange the projected rows and scores, not the source rows
+            self.exchange.exchange_tensors(proj)
+        self.kernel_launches += 2
+        return proj
 
     def _schedule(self, gl, row_ids, row_base, B, full):
         if not full:

@@ -5,8 +5,10 @@ One process per GPU (torchrun), NCCL over NVLink/NVSwitch through
 (batch invariance, glint/kernels.py:1-8), so rank k computes the contiguous
 node range [p_k, p_{k+1}) of every full-mode layer and the only data-path
 communication is one exchange per stored layer output that a later layer
-reads: each rank broadcasts its row slice to all ranks (uneven slices, so P
-root broadcasts rather than a padded all-gather).  The model output is never
+reads: each rank broadcasts its row slice to all ranks.  The slices are
+uneven, so this is P root broadcasts rather than a padded all-gather, issued
+as ONE grouped NCCL collective (ncclGroupStart/End through torch's coalescing
+manager) per exchanged piece.  The model output is never
 exchanged; rows are gathered to the host once.
 
 Split points balance aggregation bytes, not node counts: the cost of a row is
@@ -77,11 +79,37 @@ class RowExchange:
             keys.append(key)
         return keys
 
-    def _post(self, engine, keys, upto):
+    def _group_device(self):
+        """The CUDA device to coalesce on (NCCL), or None (gloo: serial)."""
+        import torch
         import torch.distributed as dist
 
+        if dist.get_backend(self.group) != "nccl":
+            return None
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def _broadcasts(self, parts):
+        """[(tensor, root)] as ONE grouped collective on NCCL (ncclGroupStart /
+        ncclGroupEnd around the P root broadcasts: the transfers run concurrently
+        instead of one root after another); serial async broadcasts on gloo.
+        Returns the work handles."""
+        import torch.distributed as dist
+
+        parts = [(t, k) for t, k in parts if t.numel()]
+        if not parts:
+            return []
+        dev = self._group_device()
+        if dev is None:
+            return [dist.broadcast(t, src=k, group=self.group, async_op=True) for t, k in parts]
+        with dist._coalescing_manager(group=self.group, device=dev, async_ops=True) as cm:
+            for t, k in parts:
+                dist.broadcast(t, src=k, group=self.group, async_op=True)
+        return [cm]
+
+    def _post(self, engine, keys, upto):
         while self._posted < upto:
             c = self._posted
+            parts = []
             for k in range(self.world):
                 lo, hi = self._piece(k, c)
                 if hi <= lo:
@@ -90,8 +118,8 @@ class RowExchange:
                     part = engine.stores[key].data[lo:hi]
                     if k == self.rank:
                         self.bytes_sent += part.numel() * part.element_size()
-                    self._works.append(dist.broadcast(part, src=k, group=self.group,
-                                                      async_op=True))
+                    parts.append((part, k))
+            self._works += self._broadcasts(parts)
             self._posted += 1
 
     def piece_bounds(self):
@@ -118,18 +146,21 @@ class RowExchange:
 
     def exchange_tensor(self, data):
         """In place: rows [cuts[k], cuts[k+1]) of `data` come from rank k."""
-        import torch.distributed as dist
+        self.exchange_tensors((data,))
 
-        works = []
+    def exchange_tensors(self, tensors):
+        """exchange_tensor over several row-aligned tensors in one grouped collective."""
+        parts = []
         for k in range(self.world):
             lo, hi = int(self.cuts[k]), int(self.cuts[k + 1])
             if hi <= lo:
                 continue
-            part = data[lo:hi]
-            if k == self.rank:
-                self.bytes_sent += part.numel() * part.element_size()
-            works.append(dist.broadcast(part, src=k, group=self.group, async_op=True))
-        for w in works:
+            for data in tensors:
+                part = data[lo:hi]
+                if k == self.rank:
+                    self.bytes_sent += part.numel() * part.element_size()
+                parts.append((part, k))
+        for w in self._broadcasts(parts):
             w.wait()
 
     def __call__(self, engine, blk):

@@ -211,8 +211,10 @@ def test_nodewise_hard_oom(golden, cuda):
 @pytest.mark.gpu
 def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
     """The torchrun path (edge-balanced row ranges + per-layer exchange) gives the
-    single-rank bytes for GCN and GAT, one batch and many batches per layer.
-    Two ranks share cuda:0 over gloo (NCCL refuses duplicate devices)."""
+    single-rank bytes for GCN (aggregate-first and reassociated) and GAT, one
+    batch and many batches per layer, and on a star graph whose edge-balanced
+    ranges leave ranks empty.  2 and 4 ranks share cuda:0 over gloo (NCCL
+    refuses duplicate devices)."""
     import json
     import os
     import pathlib
@@ -221,14 +223,18 @@ def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
 
     root = pathlib.Path(__file__).resolve().parents[1]
     env = dict(os.environ, GLINT_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533",
-           str(root / "tools" / "dist_check.py"), "20000"]
-    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
-    assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
-    assert len(lines) == 4
-    assert all(x["bit_identical_all_ranks"] for x in lines), lines
+    for world in (2, 4):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+               str(world), "--master-addr", "127.0.0.1", "--master-port", str(29533 + world),
+               str(root / "tools" / "dist_check.py"), "20000"]
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+        runs = [x for x in lines if "model" in x]
+        assert len(runs) == 6 + 3, lines
+        assert all(x["bit_identical_all_ranks"] for x in runs), runs
+        star = next(x for x in lines if "star_cuts" in x)
+        assert star["empty_ranks"] >= (world > 2)      # a rank without rows took part
 
 
 @pytest.mark.gpu

@@ -35,17 +35,40 @@ def main():
     g = synth.gen_products_like(n, und, seed=3, device="cuda")
     host = CscGraph(n, g.num_edges, np.asarray(g.indptr_host), g.indices.to(torch.int64).cpu().numpy())
     x = synth.gen_features_device(n, 100, seed=3, device="cuda").cpu().numpy()
-    for name, m in (("gcn3", synth.build_gcn(100, 256, 47, 3, seed=0)),
-                    ("gat3", synth.build_gat(100, 64, 47, 3, heads=4, seed=0))):
+    models = (("gcn3", synth.build_gcn(100, 256, 47, 3, seed=0)),
+              ("gat3", synth.build_gat(100, 64, 47, 3, heads=4, seed=0)))
+
+    def check(tag, m, hg, xx, cap, reassoc):
+        kw = dict(budget=DeviceBudget(cap), reassociate=reassoc)
+        ref = run_inference(m, hg, xx, distributed=False, **kw).output
+        out = run_inference(m, hg, xx, distributed="auto", **kw).output
+        flags = torch.tensor([1.0 if np.array_equal(ref, out) else 0.0], device="cuda")
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(json.dumps({"graph": tag, "model": name, "world": world, "nodes": hg.num_nodes,
+                              "capacity": cap, "reassociate": reassoc,
+                              "bit_identical_all_ranks": bool(flags.item() == 1.0)}), flush=True)
+
+    for name, m in models:
         for cap in (1 << 34, 64 << 20):       # one batch per layer / many batches
-            ref = run_inference(m, host, x, budget=DeviceBudget(cap), distributed=False).output
-            out = run_inference(m, host, x, budget=DeviceBudget(cap), distributed="auto").output
-            same = bool(np.array_equal(ref, out))
-            flags = torch.tensor([1.0 if same else 0.0], device="cuda")
-            dist.all_reduce(flags, op=dist.ReduceOp.MIN)
-            if rank == 0:
-                print(json.dumps({"model": name, "world": world, "nodes": n, "capacity": cap,
-                                  "bit_identical_all_ranks": bool(flags.item() == 1.0)}), flush=True)
+            for reassoc in ((False, True) if name == "gcn3" else (False,)):
+                check("products_like", m, host, x, cap, reassoc)
+    # A star: every edge points into node 0, so edge-balanced ranges leave
+    # ranks with no rows (those ranks must still join every
+    # collective of the transform-first convs).
+    from paper_2211_15082_b200.parallel import edge_balanced_ranges
+
+    ns = 20
+    star = CscGraph(ns, ns - 1, np.array([0] + [ns - 1] * ns, dtype=np.int64),
+                    np.arange(1, ns, dtype=np.int64))
+    xs = synth.gen_features(ns, 100, seed=1)
+    cuts = edge_balanced_ranges(star.indptr, world)
+    if rank == 0:
+        print(json.dumps({"star_cuts": cuts.tolist(),
+                          "empty_ranks": int(np.sum(np.diff(cuts) == 0))}), flush=True)
+    for name, m in models:
+        for reassoc in ((False, True) if name == "gcn3" else (False,)):
+            check("star", m, star, xs, 1 << 34, reassoc)
     dist.destroy_process_group()
 
 
