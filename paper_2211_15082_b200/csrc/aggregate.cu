@@ -430,6 +430,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) mean_hub_kernel(MeanArgs a, int
 struct SideStream {
   cudaStream_t stream = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  std::mutex mu;   // held from the fork record to the caller's join wait
 };
 
 // Library-internal side stream (per device) for the concurrent hub kernel.
@@ -449,6 +450,47 @@ int side_stream(SideStream** out) {
   return GLINT_OK;
 }
 
+// Fork/join of the caller's stream with the side stream.  The side stream's
+// mutex is held from the fork record until the caller's stream has enqueued
+// its wait on the join, so concurrent callers (threads, streams) cannot
+// interleave their event records; the destructor always enqueues the join,
+// so an error return after the fork never leaves the caller's stream without
+// the dependency on work already queued on the side stream.
+class SideFork {
+ public:
+  int begin(cudaStream_t caller) {
+    int rc = side_stream(&ss_);
+    if (rc) return rc;
+    lk_ = std::unique_lock<std::mutex>(ss_->mu);
+    caller_ = caller;
+    GLINT_CUDA(cudaEventRecord(ss_->fork, caller));
+    joined_ = false;
+    GLINT_CUDA(cudaStreamWaitEvent(ss_->stream, ss_->fork, 0));
+    return GLINT_OK;
+  }
+  cudaStream_t stream() const { return ss_->stream; }
+  int join() {
+    if (joined_) return GLINT_OK;
+    joined_ = true;
+    cudaError_t e1 = cudaEventRecord(ss_->join, ss_->stream);
+    cudaError_t e2 = cudaStreamWaitEvent(caller_, ss_->join, 0);
+    lk_.unlock();
+    cudaError_t e = e1 != cudaSuccess ? e1 : e2;
+    if (e != cudaSuccess) {
+      set_error("side stream join failed: %s", cudaGetErrorString(e));
+      return GLINT_ECUDA;
+    }
+    return GLINT_OK;
+  }
+  ~SideFork() { join(); }
+
+ private:
+  SideStream* ss_ = nullptr;
+  cudaStream_t caller_ = nullptr;
+  std::unique_lock<std::mutex> lk_;
+  bool joined_ = true;
+};
+
 template <int CW>
 int launch_hub_cw(const MeanArgs& a, bool bulk, cudaStream_t s) {
   // slices of <= 32*CW columns per CTA (several CTAs per hub row keep more
@@ -460,11 +502,11 @@ int launch_hub_cw(const MeanArgs& a, bool bulk, cudaStream_t s) {
   int per_group = kHubRingBytes / (slice_floats * 4) / kHubGroups;
   per_group = std::max(1, std::min(per_group, 32));  // one producer lane per slot
   const int smem = per_group * kHubGroups * slice_floats * 4;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(mean_hub_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kHubRingBytes + 4096));
-    configured = true;
+    configured.mark();
   }
   const int64_t grid = a.sc.n_hub * col_blocks;
   mean_hub_kernel<CW><<<static_cast<unsigned>(grid), (CW + 1) * 32, smem, s>>>(
@@ -645,11 +687,11 @@ __global__ void __launch_bounds__(32) mean_hub_async_kernel(MeanArgs a, int col_
 
 int launch_hub_async(const MeanArgs& a, cudaStream_t s) {
   constexpr int smem = kHubR * 32 * 16;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(mean_hub_async_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured.mark();
   }
   const int col_blocks = static_cast<int>(ceil_div(a.dim, 128));
   const int64_t units = a.sc.n_hub * col_blocks;
@@ -663,13 +705,13 @@ template <int LPR, int VPL, int R, int MINB, int B = 1>
 int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
   constexpr int G = 32 / LPR;
   constexpr int smem = R * VPL * kThreads * 16;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured.mark();
   }
   const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
   if (grid <= 0) return GLINT_OK;
@@ -720,15 +762,13 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
     mean_hub_reg_kernel<<<static_cast<unsigned>(a.sc.hub_ctas), kThreads, 0, s>>>(a);
     return launch_status("spmm_mean_hub");
   }
-  SideStream* ss = nullptr;
-  int rc = side_stream(&ss);
+  SideFork fork;
+  int rc = fork.begin(s);
   if (rc) return rc;
-  GLINT_CUDA(cudaEventRecord(ss->fork, s));
-  GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
   if (vec4 && knob == 5) {
-    rc = launch_hub_async(a, ss->stream);
+    rc = launch_hub_async(a, fork.stream());
   } else if (vec4 && (knob >= 2 || (knob == 0 && a.sc.n_rows < (1 << 19)))) {
-    rc = launch_hub(a, ss->stream);
+    rc = launch_hub(a, fork.stream());
   } else {
     // CTAs per SM for the register hub kernel: knob 6 = k caps the grid at
     // k CTAs per SM (persistent); 0 (default) = one CTA per unit, measured
@@ -736,14 +776,13 @@ int dispatch_mean(const MeanArgs& a, bool vec4, cudaStream_t s) {
     const int per_sm = tuning(GLINT_TUNE_HUB_CTAS_PER_SM);
     const int64_t cap = per_sm == 0 ? a.sc.hub_ctas : static_cast<int64_t>(per_sm) * sm_count();
     const int64_t grid = std::min<int64_t>(a.sc.hub_ctas, cap);
-    mean_hub_reg_kernel<<<static_cast<unsigned>(grid), kThreads, 0, ss->stream>>>(a);
+    mean_hub_reg_kernel<<<static_cast<unsigned>(grid), kThreads, 0, fork.stream()>>>(a);
     rc = launch_status("spmm_mean_hub");
   }
   if (rc) return rc;
-  GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   rc = dispatch_regular(a, vec4, s);
-  GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
-  return rc;
+  const int rj = fork.join();
+  return rc ? rc : rj;
 }
 
 int dispatch_regular(const MeanArgs& a, bool vec4, cudaStream_t s) {
@@ -1699,12 +1738,12 @@ int launch_gat_hub_ring_cw(const GatArgs& a, cudaStream_t s) {
   // weight chunks must cover whole ring groups
   while (kGatWChunk % per_group) --per_group;
   const int smem = per_group * kHubGroups * slice_floats * 4 + kGatWChunk * a.heads * 4;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(gat_hub_ring_kernel<CW>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kHubRingBytes + kGatWChunk * kMaxHeads * 4));
-    configured = true;
+    configured.mark();
   }
   const int64_t grid = a.sc.n_hub * col_blocks;
   // TMA bulk copies by default (one 512 B request per source row slice;
@@ -1758,26 +1797,23 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
     }
     return launch_gat_hub_ring(a, hs);
   };
-  SideStream* ss = nullptr;
+  SideFork fork;
   if (a.sc.hub_ctas > 0 && !after) {
     // hub CTAs on the library side stream, concurrent with the regular rows
-    int rc = side_stream(&ss);
+    int rc = fork.begin(s);
     if (rc) return rc;
-    GLINT_CUDA(cudaEventRecord(ss->fork, s));
-    GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-    rc = launch_hubs(ss->stream);
+    rc = launch_hubs(fork.stream());
     if (rc) return rc;
-    GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   }
   if constexpr (R == 0) {
     if (grid > 0) gat_kernel<H, LPR, VPL, U, MINB><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
   } else {
     constexpr int smem = R * VPL * kThreads * 16 + kThreads * H * 4;  // Z ring + chunk weights
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    if (configured.needed()) {
       GLINT_CUDA(cudaFuncSetAttribute(gat_async_kernel<H, LPR, VPL, R, MINB>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured = true;
+      configured.mark();
     }
     if (grid > 0)
       gat_async_kernel<H, LPR, VPL, R, MINB><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
@@ -1785,23 +1821,19 @@ int launch_gat(const GatArgs& a, cudaStream_t s) {
   int rc = launch_status("gat_aggregate");
   if (rc) return rc;
   if (a.sc.hub_ctas > 0 && after) return launch_hubs(s);
-  if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
-  return rc;
+  return fork.join();
 }
 
 // Two-phase GAT launch: hub rows on the side stream (one-phase ring kernel),
 // regular rows as edge softmax then weighted SpMM on the caller's stream.
 template <int H, int LPR_A, int LPR, int VPL, int R, int MINB>
 int launch_gat2(const GatArgs& a, cudaStream_t s) {
-  SideStream* ss = nullptr;
+  SideFork fork;
   if (a.sc.hub_ctas > 0) {
-    int rc = side_stream(&ss);
+    int rc = fork.begin(s);
     if (rc) return rc;
-    GLINT_CUDA(cudaEventRecord(ss->fork, s));
-    GLINT_CUDA(cudaStreamWaitEvent(ss->stream, ss->fork, 0));
-    rc = launch_gat_hub_ring(a, ss->stream);
+    rc = launch_gat_hub_ring(a, fork.stream());
     if (rc) return rc;
-    GLINT_CUDA(cudaEventRecord(ss->join, ss->stream));
   }
   const int64_t regular = a.sc.n_rows - a.sc.n_hub;
   if (regular > 0) {
@@ -1810,18 +1842,18 @@ int launch_gat2(const GatArgs& a, cudaStream_t s) {
     int rc = launch_status("gat_softmax");
     if (rc) return rc;
     constexpr int smem = R * VPL * kThreads * 16;
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    if (configured.needed()) {
       GLINT_CUDA(cudaFuncSetAttribute(gat_spmm_async_kernel<H, LPR, VPL, R, MINB>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured = true;
+      configured.mark();
     }
     const int64_t gb = ceil_div(regular, kWarps * (32 / LPR));
     gat_spmm_async_kernel<H, LPR, VPL, R, MINB><<<static_cast<unsigned>(gb), kThreads, smem, s>>>(a);
   }
   const int rc = launch_status("gat_spmm");
-  if (a.sc.hub_ctas > 0) GLINT_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
-  return rc;
+  const int rj = fork.join();
+  return rc ? rc : rj;
 }
 
 // chunks = 128-bit chunks per padded Z row.  Variants (GLINT_TUNE_GAT_VARIANT)

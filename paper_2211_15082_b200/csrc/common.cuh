@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "../../include/glint_b200.h"
 
@@ -30,6 +31,20 @@ int sm_count();  // cached per current device
 int tuning(int key);  // glint_set_tuning knobs (0 = default behaviour)
 
 constexpr int kWarp = 32;
+
+// Once-per-device guard for host-side kernel configuration
+// (cudaFuncSetAttribute is a per-device property; a process-wide flag would
+// skip it on the second device a process uses).  Idempotent under races.
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  static uint64_t bit() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 1ull << (dev & 63);
+  }
+  bool needed() const { return (done.load(std::memory_order_acquire) & bit()) == 0; }
+  void mark() { done.fetch_or(bit(), std::memory_order_release); }
+};
 
 }  // namespace glint
 

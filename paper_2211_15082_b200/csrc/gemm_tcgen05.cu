@@ -461,11 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_3xtf32_kernel(TcArgs a) {
 template <int BN, bool VEC, int ACT>
 int launch_tc(TcArgs a, cudaStream_t s) {
   using C = Cfg<BN>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(gemm_3xtf32_kernel<BN, VEC, ACT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    configured = true;
+    configured.mark();
   }
   a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
   a.num_tiles = ceil_div(a.M, BM) * a.n_tiles;
@@ -956,11 +956,11 @@ int launch_v2(TcArgs a, cudaStream_t s) {
   using C = Cfg2<BN, MH>;
   constexpr int smem = SC ? C::SMEM_SC : C::SMEM;
   static_assert(smem <= 227 * 1024, "v2 GEMM shared memory over the per-CTA limit");
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
     GLINT_CUDA(cudaFuncSetAttribute(gemm_v2_kernel<BN, ACT, SC, MH>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured.mark();
   }
   a.n_tiles = static_cast<int>(ceil_div(a.N, BN));
   a.num_tiles = ceil_div(a.M, C::TM) * a.n_tiles;

@@ -35,7 +35,7 @@ import numpy as np
 
 from . import _lib, device as devmodel, kernels
 from .batching import BatchController, Thresholds
-from .errors import ConfigError, DeviceCapacityError, InternalError
+from .errors import ConfigError, DeviceAllocationError, DeviceCapacityError, InternalError
 from .model_ir import ModelGraph
 from .reorder import NodeOrder, apply_order_device, make_order
 from .splitter import INPUT_REF, BlockSchedule, TensorRef, split
@@ -702,9 +702,15 @@ class LayerwiseEngine:
                                           self.dims), self.budget)):
             if self.probe is not None:
                 self.probe.mark(f"L{layer} whole layer [{lo},{hi})")
-            run_rows(lo, hi, n_nodes)
-            spec["hi"] = hi
-            speculate = True
+            try:
+                run_rows(lo, hi, n_nodes)
+                spec["hi"] = hi
+                speculate = True
+            except torch.cuda.OutOfMemoryError:
+                # the real allocator disagrees with the footprint model: fall
+                # back to the controller's batches (rows done so far are valid
+                # and are recomputed with the same bytes)
+                torch.cuda.empty_cache()
 
         def execute(plan: _Plan):
             if self.probe is not None:
@@ -712,7 +718,11 @@ class LayerwiseEngine:
             self._batch_hubs = plan.num_hubs
             r0 = max(plan.start, spec["hi"]) if speculate else plan.start
             if r0 < plan.end:
-                run_rows(r0, plan.end, plan.num_inputs)
+                try:
+                    run_rows(r0, plan.end, plan.num_inputs)
+                except torch.cuda.OutOfMemoryError as exc:   # -> controller on_oom
+                    torch.cuda.empty_cache()
+                    raise DeviceAllocationError(str(exc).splitlines()[0]) from exc
 
         if full:
             self.plan_stream.wait_event(gl.indptr_event)     # planning reads only the CSR
@@ -725,8 +735,15 @@ class LayerwiseEngine:
         def plan_off(start, end):
             a, b = start + lo, end + lo
             if speculate and b > spec["hi"]:
-                run_rows(max(a, spec["hi"]), b, b - a)
-                spec["hi"] = b
+                # Only a batch the footprint model is sure to admit runs ahead
+                # of its count: n_inputs <= min(N, n_targets + n_edges) bounds
+                # the footprint from above, so the budget holds during uploads.
+                n_e = int(prefix[b] - prefix[a])
+                bound = devmodel.footprint_counts(blk, b - a, min(n_nodes, (b - a) + n_e), n_e,
+                                                  self.dims)
+                if devmodel.admit(bound, self.budget):
+                    run_rows(max(a, spec["hi"]), b, b - a)
+                    spec["hi"] = b
             plan, fp = plan_fn(a, b)
             return plan, fp
 

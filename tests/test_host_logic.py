@@ -184,6 +184,33 @@ def test_controller_unrecoverable_singleton():
                       lambda p: None)
 
 
+def test_controller_real_allocation_failure_halves_and_retries():
+    """A DeviceAllocationError while an admitted batch executes is on_oom: the
+    thresholds halve, the same cursor is re-planned, the retry is recorded."""
+    from paper_2211_15082_b200.errors import DeviceAllocationError
+
+    ctl = batching.BatchController(batching.Thresholds(8, 10 ** 6), DeviceBudget(10 ** 9))
+    prefix = np.arange(33, dtype=np.int64)
+    ran = []
+
+    def execute(plan):
+        s, e = plan
+        if e - s > 2:                      # the device refuses anything above 2 rows
+            raise DeviceAllocationError("cudaErrorMemoryAllocation")
+        ran.append(plan)
+
+    recs = ctl.run_layer(1, np.arange(32), prefix,
+                         lambda s, e: ((s, e), BatchFootprint(0, 0, 1, 0)), execute)
+    assert recs[0].start == 0 and recs[0].end == 2 and recs[0].oom_retries == 2
+    assert [(r.start, r.end) for r in recs] == ran
+    assert sum(r.n_targets for r in recs) == 32
+    with pytest.raises(DeviceCapacityError):
+        ctl2 = batching.BatchController(batching.Thresholds(1, 10), DeviceBudget(10 ** 9))
+        ctl2.run_layer(1, np.arange(3), np.arange(4),
+                       lambda s, e: ((s, e), BatchFootprint(0, 0, 1, 0)),
+                       lambda p: (_ for _ in ()).throw(DeviceAllocationError("oom")))
+
+
 def test_adapt_half_even_rounding():
     t = batching.adapt(batching.Thresholds(5, 5), 900, 1800)  # r = 0.5 -> round(2.5) = 2
     assert (t.n_t, t.n_i) == (2, 2)
