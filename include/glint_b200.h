@@ -91,6 +91,10 @@ int glint_abi_version(void);
                                      N/2; N <= 128: 3 = 128-row tiles */
 #define GLINT_TUNE_HUB_AFTER 8    /* hub-row kernels: 0 concurrent (side stream), 1 after
                                      the regular rows on the caller's stream */
+#define GLINT_TUNE_GEMM_V3 9     /* K2/K3: 0 v3 (tensor-map TMA, CTA pairs) where the
+                                     shape allows, 1 the v2 kernel */
+#define GLINT_TUNE_GEMM_PF 10    /* v3 K2: L2 prefetch of A, tiles ahead (0 default = 1,
+                                     -1 off) */
 #define GLINT_TUNE_COUNT 12
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);

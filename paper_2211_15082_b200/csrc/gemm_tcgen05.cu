@@ -29,6 +29,8 @@
 //
 // Row invariance (kernels.py:1-14): an output row depends only on its own A
 // row and W with a fixed k order, so any batching of rows gives equal bytes.
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace glint {
@@ -1030,6 +1032,705 @@ int launch_v2_scores(const TcArgs& a, cudaStream_t s) {
 
 }  // namespace v2
 
+// ============================================================== v3 kernel --
+//
+// Same split-TF32 products, k order and epilogue as v2, with the operand path
+// rebuilt around the Blackwell copy engines:
+//   * A and W tiles arrive by TMA tensor copies (cp.async.bulk.tensor, SASS
+//     UTMALDG) into the 128-byte-swizzled K-major UMMA layout: 32 fp32 of K
+//     per row per chunk (one swizzle atom row), 8-row groups 1 KB apart.  One
+//     elected thread issues every copy, so no warp spends issue slots on
+//     address generation (v2's 8 LDGSTS producer warps).
+//   * The raw fp32 tile is the TF32 "hi" operand (the tensor core ignores the
+//     low 13 mantissa bits, tools/tf32_trunc_probe.py).  Four converter warps
+//     compute lo = x - trunc(x) elementwise over the same swizzled bytes (the
+//     layout is a byte permutation, so lo lands in the identical layout), for
+//     A and for W: no W panel kernel, no workspace, no allocation.
+//   * N > 64: a CTA pair (cluster of 2, tcgen05 cta_group::2).  The pair
+//     computes a 256-row tile with one M = 256 MMA per product; each CTA
+//     loads its own 128 A rows and HALF of the W rows (B split along N across
+//     the pair, tools/probes/umma2_probe.cu), which halves the per-SM W traffic
+//     from L2 and the shared-memory B reads.  The leader's thread issues the
+//     MMAs and commits to both CTAs' barriers (multicast); the peer's
+//     converters and epilogue warps arrive on the leader's barriers remotely.
+//   * N <= 64 (the narrowing layer-3 transform, 256 -> 47): W (raw + lo) stays
+//     resident in shared memory for the whole persistent CTA, so only A
+//     streams and the kernel runs at the A-read (HBM) rate.
+//   * TMEM holds two accumulators: the MMA issuer starts tile i+1 while the
+//     epilogue warps drain tile i.
+namespace v3 {
+
+constexpr int BKC = 32;                     // fp32 K per chunk = one 128 B swizzle row
+constexpr int ROWS = 128;                   // A rows per CTA per tile
+constexpr int A_BYTES = ROWS * BKC * 4;     // 16 KB
+constexpr int NCONV = 4;                    // converter warps per group (one per lane quarter)
+// One converter group: a second group taking alternate chunks measured no
+// faster, and with an odd stage count two consumers of one stage ring make
+// the mbarrier parity waits ambiguous (a waiter can see the previous phase of
+// the same parity as complete) -- tools/gemm_det_check.py caught exactly that.
+constexpr int NGRP = 1;
+constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, W_EPI = W_CONV + NGRP * NCONV;
+// epilogue warps: 4 (one per TMEM lane quarter); the GAT score epilogue uses
+// 8 (two per quarter, split at a head boundary: its per-row score chains are
+// the long pole there)
+template <bool SC>
+constexpr int nepi() { return SC ? 8 : 4; }
+template <bool SC>
+constexpr int threads3() { return (W_EPI + nepi<SC>()) * 32; }
+constexpr int RL = 2;                       // A lo ring depth (shared memory, pair kernels)
+constexpr int RT = 4;                       // A hi/lo TMEM slots (resident-W kernels)
+constexpr uint32_t TS_BASE = 256;           // first TMEM column of the A slots
+constexpr int MAX_RS = 8;
+constexpr int SMEM_CAP = 227 * 1024 - 2048;   // dynamic budget: 227 KB less the static barriers
+constexpr uint64_t POLICY_EVICT_FIRST = 0x12F0000000000000ull;
+constexpr uint64_t POLICY_EVICT_LAST = 0x14F0000000000000ull;
+
+template <int BN, bool PAIR>
+struct Cfg3 {
+  static constexpr int BNH = PAIR ? BN / 2 : BN;     // W rows one CTA holds
+  static constexpr int WB = BNH * BKC * 4;           // one W chunk (raw or lo)
+  static constexpr uint32_t TCOLS = PAIR ? (2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128
+                                             ? 128 : 2 * BN <= 256 ? 256 : 512)
+                                         : 512;   // single CTAs: accumulators + A slots
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>((PAIR ? 2 * ROWS : ROWS) >> 4) << 24);
+  static_assert(BNH % 8 == 0, "W rows per CTA must fill 8-row swizzle groups");
+  static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
+};
+
+// Shared-memory plan (dynamic, every buffer 1 KB aligned for the swizzle):
+//   [RS stages: A raw | W raw | W lo (streamed W only)] [RL A lo] [resident W
+//   raw/lo chunks] [epilogue staging | bias | score tables]
+struct Plan3 {
+  int rs = 0, stage = 0, lo_off = 0, wres_off = 0, epi_off = 0, smem = 0;
+};
+
+// staging tiles + per-warp bias copies + score tables
+template <int BN, bool SC>
+constexpr int epi_bytes() {
+  return nepi<SC>() * (32 * EPI_LD + BN) * 4 + (SC ? 3 * v2::kScMaxN * 4 : 0);
+}
+
+template <int BN, bool PAIR, bool RESW, bool SC>
+Plan3 plan3(int nkc) {
+  using C = Cfg3<BN, PAIR>;
+  constexpr int EPI = epi_bytes<BN, SC>();
+  Plan3 p;
+  p.stage = A_BYTES + (RESW ? 0 : 2 * C::WB);
+  const int wres = RESW ? nkc * 2 * C::WB : 0;
+  // resident-W kernels keep A hi/lo in TMEM, so only the pair kernels need
+  // the shared-memory lo ring
+  const int fixed = (RESW ? 0 : RL * A_BYTES) + wres + EPI + 1024;   // +1 KB align slack
+  p.rs = std::min(MAX_RS, (SMEM_CAP - fixed) / p.stage);
+  p.lo_off = p.rs * p.stage;
+  p.wres_off = p.lo_off + (RESW ? 0 : RL * A_BYTES);
+  p.epi_off = p.wres_off + wres;
+  p.smem = p.epi_off + EPI + 1024;
+  return p;
+}
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;                   // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;           // SBO: 8-row groups 1 KB apart
+  d |= static_cast<uint64_t>(1) << 46;                   // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;                   // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t num_clusters() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+
+// arrive on the pair leader's copy of `bar` (CTA rank 0 of the cluster)
+template <bool PAIR>
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t rank) {
+  // default (.release.cta) semantics, as CUTLASS's ClusterBarrier: a
+  // .cluster-scope release compiles to MEMBAR.GPU + L1 invalidation (CCTL.IVALL)
+  // per arrive, measured as ~23% of the stall samples of the first v3 build
+  if (!PAIR || rank == 0) {
+    mbar_arrive(bar);
+  } else {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_addr(bar)));
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar)),
+        "l"(policy)
+      : "memory");
+}
+
+// L2 prefetch of one box (no shared memory, no barrier): tiles ahead of the
+// shared-memory ring, so the ring's TMA loads hit L2
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
+}
+
+// The MMA issuer is a whole warp running a convergent loop over warp-uniform
+// values; elect.sync INSIDE the asm picks the one issuing lane.  With the
+// instruction descriptor an immediate and the k-steps unrolled at constant
+// descriptor offsets, the compiler keeps every operand in uniform registers:
+// tools/probes/mma_rate_probe.cu measures this form at the M*N/256-cycle
+// formula (TS: 24 cycles at N = 48), where a lane-0-only loop with a runtime
+// descriptor cost ~100 cycles per MMA (R2UR + ELECT waterfall per issue).
+template <bool PAIR, uint32_t IDESC>
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  if constexpr (PAIR) {
+    asm volatile(
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %3, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %4, p;\n}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(accumulate), "n"(IDESC));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %3, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(accumulate), "n"(IDESC));
+  }
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n}\n"
+      ::"r"(d), "r"(a_tmem), "l"(b), "r"(accumulate), "n"(IDESC));
+}
+
+// tcgen05.commit (one elected lane) to `bar` in this CTA or in both CTAs of the pair
+template <bool PAIR>
+__device__ __forceinline__ void commit3(uint64_t* bar) {
+  if constexpr (PAIR) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n}\n" ::"r"(smem_addr(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
+        ::"r"(smem_addr(bar)) : "memory");
+  }
+}
+
+// lo = x - trunc_tf32(x) over n16 16-byte words (same byte offsets)
+__device__ __forceinline__ float lo_of(float v) {
+  return __fsub_rn(v, __uint_as_float(__float_as_uint(v) & 0xFFFFE000u));
+}
+__device__ __forceinline__ float4 lo_of(float4 v) {
+  return make_float4(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w));
+}
+// four loads in flight per thread before the dependent math and stores
+__device__ __forceinline__ void split_lo(const uint8_t* src, uint8_t* dst, int n16, int t) {
+  constexpr int T = NCONV * 32;
+  int q = t;
+  for (; q + 3 * T < n16; q += 4 * T) {
+    float4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const float4*>(src + (q + i * T) * 16);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) *reinterpret_cast<float4*>(dst + (q + i * T) * 16) = lo_of(v[i]);
+  }
+  for (; q < n16; q += T)
+    *reinterpret_cast<float4*>(dst + q * 16) = lo_of(*reinterpret_cast<const float4*>(src + q * 16));
+}
+
+// tcgen05.st of 32 consecutive TMEM columns of this warp's lane quarter
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+        "f"(v[7]), "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]),
+        "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]),
+        "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+// A operand from TMEM (the "TS" form): D[tmem] += A[tmem] . B[smem]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+struct V3Args {
+  int rs, stage, lo_off, wres_off, epi_off;
+  int nkc;              // K chunks of 32
+  int pf_tiles;         // L2 prefetch distance of A, in this CTA's tiles (0 = off)
+  int n_tiles;          // column tiles of BN
+  int64_t num_tiles;    // m tiles (of 128 or 256 rows) x n tiles
+};
+
+template <int BN, int ACT, bool SC, bool PAIR, bool RESW>
+__global__ void __launch_bounds__(threads3<SC>(), 1)
+gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+               TcArgs a, V3Args g) {
+  using C = Cfg3<BN, PAIR>;
+  constexpr int NEPI = nepi<SC>();
+  extern __shared__ uint8_t smem_raw[];
+  // 1 KB alignment for the 128 B swizzle atoms
+  // (offset arithmetic on the __shared__ array keeps the state-space provenance,
+  // so the converters and the epilogue get LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full[MAX_RS], empty[MAX_RS], rdy[MAX_RS];
+  __shared__ __align__(8) uint64_t lo_empty[RT];   // A lo slots (RL) or A TMEM slots (RT)
+  __shared__ __align__(8) uint64_t tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t wres_full, wres_rdy;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cta_rank() : 0;
+  const uint32_t cid = PAIR ? cluster_id() : blockIdx.x;
+  const uint32_t ncl = PAIR ? num_clusters() : gridDim.x;
+  constexpr uint32_t NPEER = PAIR ? 2 : 1;
+  const int rs = g.rs;
+
+  if (warp == W_MMA) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_addr(&tmem_slot)), "r"(C::TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_addr(&tmem_slot)), "r"(C::TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    for (int i = 0; i < rs; ++i) {
+      mbar_init(&full[i], 1);                 // producer arrive + TMA bytes
+      mbar_init(&empty[i], RESW ? NCONV : 1);  // converters (A now in TMEM) or MMA commit
+      mbar_init(&rdy[i], NCONV * NPEER);      // converters of both CTAs (leader's copy)
+    }
+    for (int i = 0; i < (RESW ? RT : RL); ++i) mbar_init(&lo_empty[i], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], NEPI * NPEER);
+    }
+    mbar_init(&wres_full, 1);
+    mbar_init(&wres_rdy, NGRP * NCONV);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int nkc = g.nkc;
+  const int64_t my_tiles = cid < g.num_tiles ? (g.num_tiles - 1 - cid) / ncl + 1 : 0;
+  const int64_t total = my_tiles * nkc;
+  constexpr int TM = PAIR ? 2 * ROWS : ROWS;   // rows per (pair) tile
+
+  if (warp == W_TMA) {
+    // ------------------------------------------------------------ TMA issue
+    if (lane == 0) {
+      if constexpr (RESW) {
+        v2::mbar_arrive_expect_tx(&wres_full, static_cast<uint32_t>(nkc * C::WB));
+        for (int c = 0; c < nkc; ++c)
+          tma_load_2d(smem_addr(smem + g.wres_off + c * 2 * C::WB), &tmW, c * BKC, 0, &wres_full,
+                      POLICY_EVICT_LAST);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t tile = cid;
+      int c = 0;
+      for (int64_t idx = 0; idx < total; ++idx) {
+        if (c == 0 && g.pf_tiles > 0) {
+          // this CTA's A rows of tile + pf_tiles * ncl into L2
+          const int64_t pt = tile + static_cast<int64_t>(g.pf_tiles) * ncl;
+          if (pt < g.num_tiles && (pt % g.n_tiles) == 0) {
+            const int pm = static_cast<int>((pt / g.n_tiles) * TM + rank * ROWS);
+            for (int k = 0; k < nkc; ++k) tma_prefetch_2d(&tmA, k * BKC, pm);
+          }
+        }
+        mbar_wait(&empty[s], ph ^ 1u);
+        const int64_t m0 = (tile / g.n_tiles) * TM + rank * ROWS;
+        const int n0 = static_cast<int>(tile % g.n_tiles) * BN + static_cast<int>(rank) * C::BNH;
+        uint8_t* st = smem + s * g.stage;
+        v2::mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(A_BYTES + (RESW ? 0 : C::WB)));
+        tma_load_2d(smem_addr(st), &tmA, c * BKC, static_cast<int>(m0), &full[s],
+                    POLICY_EVICT_FIRST);
+        if constexpr (!RESW)
+          tma_load_2d(smem_addr(st + A_BYTES), &tmW, c * BKC, n0, &full[s], POLICY_EVICT_LAST);
+        if (++s == rs) { s = 0; ph ^= 1u; }
+        if (++c == nkc) { c = 0; tile += ncl; }
+      }
+      // drain: every stage's last use is released (the MMA commits target
+      // this CTA's barriers) before the CTA may exit
+      for (int64_t idx = total > rs ? total - rs : 0; idx < total; ++idx)
+        mbar_wait(&empty[idx % rs], static_cast<uint32_t>(idx / rs) & 1u);
+    }
+  } else if (warp >= W_CONV && warp < W_EPI) {
+    // ----------------------------------------------------------- converters
+    const int grp = (warp - W_CONV) / NCONV;
+    const int t = threadIdx.x - (W_CONV + grp * NCONV) * 32;   // thread within the group
+    if constexpr (RESW) {
+      mbar_wait(&wres_full, 0);
+      for (int c = grp; c < nkc; c += NGRP)
+        split_lo(smem + g.wres_off + c * 2 * C::WB, smem + g.wres_off + c * 2 * C::WB + C::WB,
+                 C::WB / 16, t);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wres_rdy);
+    }
+    constexpr int NL = RESW ? RT : RL;
+    for (int64_t idx = grp; idx < total; idx += NGRP) {
+      const int s = static_cast<int>(idx % rs);
+      const uint32_t ph = static_cast<uint32_t>(idx / rs) & 1u;
+      const int l = static_cast<int>(idx % NL);
+      const uint32_t lph = static_cast<uint32_t>(idx / NL) & 1u;
+      mbar_wait(&full[s], ph);
+      mbar_wait(&lo_empty[l], lph ^ 1u);
+      uint8_t* st = smem + s * g.stage;
+      if constexpr (RESW) {
+        // thread = A row (this warp's TMEM lane quarter): read the row's 32
+        // floats out of the swizzled tile, release the stage to the TMA at
+        // once, then store hi (= raw) and lo into the TMEM slot
+        const int row = (warp & 3) * 32 + lane;
+        const uint8_t* rp = st + row * 128;
+        float v[32];
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {
+          const float4 x = *reinterpret_cast<const float4*>(rp + ((c16 ^ (row & 7)) << 4));
+          v[4 * c16] = x.x;
+          v[4 * c16 + 1] = x.y;
+          v[4 * c16 + 2] = x.z;
+          v[4 * c16 + 3] = x.w;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const uint32_t ta = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + TS_BASE +
+                            static_cast<uint32_t>(l * 64);
+        tmem_st32(ta, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = lo_of(v[i]);
+        tmem_st32(ta + 32, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_before();
+      } else {
+        split_lo(st, smem + g.lo_off + l * A_BYTES, A_BYTES / 16, t);
+        split_lo(st + A_BYTES, st + A_BYTES + C::WB, C::WB / 16, t);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      __syncwarp();
+      if (lane == 0) arrive_leader<PAIR>(&rdy[s], rank);
+    }
+    // drain the lo slots (their last commits target this CTA's barriers)
+    for (int64_t idx = total > NL ? total - NL : 0; idx < total; ++idx)
+      if (idx % NGRP == grp) mbar_wait(&lo_empty[idx % NL], static_cast<uint32_t>(idx / NL) & 1u);
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------------ MMA issue
+    if (!PAIR || rank == 0) {
+      if constexpr (RESW) mbar_wait(&wres_rdy, 0);
+      int s = 0, l = 0;
+      uint32_t ph = 0;
+      int64_t it = 0;
+      for (int64_t tile = cid; tile < g.num_tiles; tile += ncl, ++it) {
+        const int buf = static_cast<int>(it & 1);
+        mbar_wait(&tempty[buf], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+        fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * BN);
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&rdy[s], ph);
+          fence_after();
+          {
+            const uint8_t* st = smem + s * g.stage;
+            const uint32_t w_hi = RESW ? smem_addr(smem + g.wres_off + c * 2 * C::WB)
+                                       : smem_addr(st + A_BYTES);
+            const uint64_t dwh = desc_sw128(w_hi);
+            const uint64_t dwl = desc_sw128(w_hi + C::WB);
+            const int nks = min(BKC / 8, (a.K - c * BKC + 7) / 8);
+            const uint32_t acc0 = c != 0;
+            if constexpr (RESW) {
+              const uint32_t ta = tmem + TS_BASE + static_cast<uint32_t>(l * 64);
+#pragma unroll
+              for (int j = 0; j < BKC / 8; ++j) {
+                if (j < nks) {   // descriptor start address advances 32 B per k-step
+                  mma_ts<C::IDESC>(d, ta + 32 + 8 * j, dwh + 2 * j, acc0 | j);
+                  mma_ts<C::IDESC>(d, ta + 8 * j, dwl + 2 * j, 1u);
+                  mma_ts<C::IDESC>(d, ta + 8 * j, dwh + 2 * j, 1u);
+                }
+              }
+              commit3<false>(&lo_empty[l]);
+            } else {
+              const uint64_t dah = desc_sw128(smem_addr(st));
+              const uint64_t dal = desc_sw128(smem_addr(smem + g.lo_off + l * A_BYTES));
+#pragma unroll
+              for (int j = 0; j < BKC / 8; ++j) {
+                if (j < nks) {
+                  mma_ss<PAIR, C::IDESC>(d, dal + 2 * j, dwh + 2 * j, acc0 | j);
+                  mma_ss<PAIR, C::IDESC>(d, dah + 2 * j, dwl + 2 * j, 1u);
+                  mma_ss<PAIR, C::IDESC>(d, dah + 2 * j, dwh + 2 * j, 1u);
+                }
+              }
+              commit3<PAIR>(&empty[s]);
+              commit3<PAIR>(&lo_empty[l]);
+            }
+            if (c == nkc - 1) commit3<PAIR>(&tfull[buf]);
+          }
+          __syncwarp();
+          if (++s == rs) { s = 0; ph ^= 1u; }
+          if (++l == (RESW ? RT : RL)) l = 0;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    // warp (q, p): TMEM lane quarter q (the tcgen05.ld access rule), column
+    // part p: halves of BN (multiples of 16), or for the GAT score epilogue
+    // the first / last ceil(H/2) heads; a part that cannot split runs on p = 0
+    const int q = warp & 3;
+    const int p = (warp - W_EPI) >> 2;
+    float* epi = reinterpret_cast<float*>(smem + g.epi_off);
+    float* stage = epi + (warp - W_EPI) * 32 * EPI_LD;
+    float* bias_s = epi + NEPI * 32 * EPI_LD + (warp - W_EPI) * BN;
+    float* sc_tab = epi + NEPI * (32 * EPI_LD + BN);
+    const bool has_bias = a.bias != nullptr;
+    int bias_n0 = -1;
+    int cbeg = 0, cend = BN;
+    if constexpr (SC) {
+      const int split = ((a.heads + 1) / 2) * a.head_pitch;
+      if (split % 16 == 0 && split < BN) {
+        cbeg = p ? split : 0;
+        cend = p ? BN : split;
+      } else if (p) {
+        cend = 0;
+      }
+      for (int c = threadIdx.x - W_EPI * 32; c < a.N; c += NEPI * 32) {
+        const int hh = c / a.head_pitch;
+        const int j = c - hh * a.head_pitch;
+        const bool live = hh < a.heads && j < a.head_dim;
+        sc_tab[c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + j) : 0.0f;
+        sc_tab[v2::kScMaxN + c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + a.head_dim + j) : 0.0f;
+        sc_tab[2 * v2::kScMaxN + c] = __int_as_float(min(hh, a.heads - 1));
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
+    } else if constexpr (NEPI == 8) {
+      constexpr int HALF_BN = BN / 2;
+      if constexpr (HALF_BN % 16 == 0) {
+        cbeg = p * HALF_BN;
+        cend = cbeg + HALF_BN;
+      } else {
+        if (p) cend = 0;
+      }
+    }
+    int64_t it = 0;
+    for (int64_t tile = cid; tile < g.num_tiles; tile += ncl, ++it) {
+      const int buf = static_cast<int>(it & 1);
+      const int64_t m0 = (tile / g.n_tiles) * TM + rank * ROWS;
+      const int n0 = static_cast<int>(tile % g.n_tiles) * BN;
+      if (has_bias && n0 != bias_n0) {   // this warp's copy of the tile's bias (LDS broadcasts)
+        __syncwarp();
+        for (int i = lane; i < BN; i += 32) bias_s[i] = n0 + i < a.N ? __ldg(a.bias + n0 + i) : 0.f;
+        __syncwarp();
+        bias_n0 = n0;
+      }
+      mbar_wait(&tfull[buf], static_cast<uint32_t>(it >> 1) & 1u);
+      fence_after();
+      const int64_t row_base = m0 + q * 32;
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                             static_cast<uint32_t>(buf * BN);
+      const float* bias_g = bias_s;
+      v2::ScoreAcc sa{-1, 0.0f, 0.0f};
+      if constexpr (SC) {
+#pragma unroll 1
+        for (int c0 = cbeg; c0 + 16 <= cend; c0 += 16)
+          v2::epi_chunk<16, ACT, SC>(a, tbase + c0, stage, bias_g + c0, has_bias, row_base,
+                                     n0 + c0, lane, sc_tab, sa);
+        if (cend > cbeg) v2::score_flush(a, sa, row_base + lane);
+      } else {
+        int c0 = cbeg;
+#pragma unroll 1
+        for (; c0 + 32 <= cend; c0 += 32)
+          v2::epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_g + c0, has_bias, row_base,
+                                     n0 + c0, lane, sc_tab, sa);
+        if (c0 + 16 <= cend)
+          v2::epi_chunk<16, ACT, SC>(a, tbase + c0, stage, bias_g + c0, has_bias, row_base,
+                                     n0 + c0, lane, sc_tab, sa);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader<PAIR>(&tempty[buf], rank);
+    }
+  }
+  fence_before();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
+  if (warp == W_MMA) {
+    fence_after();
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp32 map over a row-major [rows x cols] matrix with row pitch ld
+// (elements); box = 32 columns (128 B) x box_rows rows, 128 B swizzle, zero fill
+int make_map(CUtensorMap* m, const float* base, int64_t rows, int cols, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("linear: cuTensorMapEncodeTiled unavailable from the driver");
+    return GLINT_ECUDA;
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BKC), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("linear: cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%d ld=%lld", static_cast<int>(r),
+              static_cast<long long>(rows), cols, static_cast<long long>(ld));
+    return GLINT_ECUDA;
+  }
+  return GLINT_OK;
+}
+
+template <int BN, int ACT, bool SC, bool PAIR, bool RESW>
+int launch_v3(TcArgs a, cudaStream_t s) {
+  using C = Cfg3<BN, PAIR>;
+  V3Args g{};
+  g.nkc = static_cast<int>(ceil_div(a.K, BKC));
+  const Plan3 p = plan3<BN, PAIR, RESW, SC>(g.nkc);
+  if (p.rs < 2) return GLINT_EUNSUPPORTED;
+  g.rs = p.rs;
+  g.stage = p.stage;
+  g.lo_off = p.lo_off;
+  g.wres_off = p.wres_off;
+  g.epi_off = p.epi_off;
+  g.n_tiles = static_cast<int>(ceil_div(a.N, BN));
+  {
+    const int knob = tuning(GLINT_TUNE_GEMM_PF);   // 0 default (1 tile ahead), -1 off, k > 0
+    g.pf_tiles = knob < 0 ? 0 : knob == 0 ? 1 : knob;
+  }
+  constexpr int TM = PAIR ? 2 * ROWS : ROWS;
+  g.num_tiles = ceil_div(a.M, TM) * g.n_tiles;
+  CUtensorMap ma, mw;
+  int rc = make_map(&ma, a.A, a.M, a.K, a.lda, ROWS);
+  if (rc) return rc;
+  rc = make_map(&mw, a.W, a.N, a.K, a.ldw, RESW ? BN : C::BNH);
+  if (rc) return rc;
+  auto kern = gemm_v3_kernel<BN, ACT, SC, PAIR, RESW>;
+  static PerDeviceOnce configured;
+  if (configured.needed()) {
+    GLINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP));
+    configured.mark();
+  }
+  const int sms = sm_count();
+  int64_t ctas = PAIR ? std::min<int64_t>(g.num_tiles, sms / 2) * 2
+                      : std::min<int64_t>(g.num_tiles, sms);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+  cfg.blockDim = dim3(threads3<SC>());
+  cfg.dynamicSmemBytes = static_cast<size_t>(p.smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mw, a, g);
+  if (e != cudaSuccess) {
+    set_error("linear_3xtf32 (v3) launch failed: %s", cudaGetErrorString(e));
+    return GLINT_ECUDA;
+  }
+  return launch_status("linear_3xtf32_v3");
+}
+
+template <int BN, bool SC, bool PAIR, bool RESW>
+int launch_v3_act(const TcArgs& a, int act, cudaStream_t s) {
+  if constexpr (SC) {
+    return launch_v3<BN, GLINT_ACT_NONE, true, PAIR, RESW>(a, s);
+  } else {
+    if (act == GLINT_ACT_RELU) return launch_v3<BN, GLINT_ACT_RELU, false, PAIR, RESW>(a, s);
+    if (act == GLINT_ACT_LEAKY_RELU) return launch_v3<BN, GLINT_ACT_LEAKY_RELU, false, PAIR, RESW>(a, s);
+    return launch_v3<BN, GLINT_ACT_NONE, false, PAIR, RESW>(a, s);
+  }
+}
+
+// Shape dispatch.  N <= 64: single CTAs with W resident (K <= 512);
+// otherwise CTA pairs with BN = N rounded up to 64 (<= 256; wider N tiles by
+// 256).  Score epilogues need every head in one column tile (N <= 256).
+// Returns GLINT_EUNSUPPORTED when no v3 shape applies (caller uses v2).
+template <bool SC>
+int dispatch_v3(const TcArgs& a, int act, cudaStream_t s) {
+  if (a.a_rows) return GLINT_EUNSUPPORTED;   // row-gathered A: no tensor map (v2 path)
+  // short-K score projections are epilogue-bound (per-row score chains); v2's
+  // 128-row tiles measured faster there (profiles/r02_gemm_v3.jsonl)
+  if (SC && a.K < 192) return GLINT_EUNSUPPORTED;
+  if (a.N <= 64 && a.K <= 512) {
+    if (a.N <= 16) return launch_v3_act<16, SC, false, true>(a, act, s);
+    if (a.N <= 32) return launch_v3_act<32, SC, false, true>(a, act, s);
+    if (a.N <= 48) return launch_v3_act<48, SC, false, true>(a, act, s);
+    return launch_v3_act<64, SC, false, true>(a, act, s);
+  }
+  if (a.N <= 64) return launch_v3_act<64, SC, true, false>(a, act, s);
+  if (a.N <= 128) return launch_v3_act<128, SC, true, false>(a, act, s);
+  if (a.N <= 192) return launch_v3_act<192, SC, true, false>(a, act, s);
+  if (SC && a.N > 256) return GLINT_EUNSUPPORTED;
+  return launch_v3_act<256, SC, true, false>(a, act, s);
+}
+
+}  // namespace v3
+
 }  // namespace
 
 // Z = A W_pad^T (3xTF32) with s_src / s_dst computed in the epilogue; returns
@@ -1059,6 +1760,10 @@ int launch_gat_project_3xtf32(int64_t M, int heads, int head_dim, int head_pitch
   a.heads = heads;
   a.head_dim = head_dim;
   a.head_pitch = head_pitch;
+  if (tuning(GLINT_TUNE_GEMM_V3) == 0) {
+    const int rc = v3::dispatch_v3<true>(a, GLINT_ACT_NONE, s);
+    if (rc != GLINT_EUNSUPPORTED) return rc;
+  }
   return v2::launch_v2_scores(a, s);
 }
 
@@ -1088,7 +1793,12 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
     a.prof = static_cast<unsigned long long*>(p);
   }
   const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
-  // v2 (double-buffered TMEM, TMA-fed W panel) unless the knob asks for v1
+  // v3 (tensor-map TMA, CTA pairs / resident W), then v2 (row-gathered A),
+  // unless the knobs ask for an older kernel
+  if (vec && tuning(GLINT_TUNE_GEMM_V1) == 0 && tuning(GLINT_TUNE_GEMM_V3) == 0) {
+    const int rc = v3::dispatch_v3<false>(a, act, s);
+    if (rc != GLINT_EUNSUPPORTED) return rc;
+  }
   if (vec && tuning(GLINT_TUNE_GEMM_V1) == 0) return v2::launch_v2_bn(a, act, s);
   return vec ? launch_bn<true>(a, act, s) : launch_bn<false>(a, act, s);
 }

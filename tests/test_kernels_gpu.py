@@ -366,6 +366,73 @@ def test_tcgen05_3xtf32_linear(cuda, M, N, K, act):
     assert one.cpu().numpy().tobytes() == got[M // 2:M // 2 + 1].tobytes()
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 47, 100), (300, 47, 256), (1000, 256, 256), (1000, 256, 100),
+                                   (129, 300, 64), (257, 16, 3), (4096, 128, 128), (77, 48, 188),
+                                   (5000, 256, 100), (513, 172, 128), (700, 65, 40), (300, 64, 600),
+                                   (2000, 600, 36), (33, 1, 9)])
+@pytest.mark.parametrize("act", [0, 1])
+def test_tcgen05_v3_linear(cuda, M, N, K, act):
+    """The v3 GEMM (tensor-map TMA, CTA pairs for N > 64, resident W for N <= 64)
+    vs fp64: rel-L2 <= 5e-6; M/N/K tails (partial 256-row pair tiles, K not a
+    multiple of the 32-wide chunk), N > 256 (column tiles), no writes past N,
+    rows computed alone equal the batch bytes, and agreement with v2."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(M * 11 + N * 3 + K + act)
+    x = rng.normal(size=(M, K)).astype(np.float32)
+    w = (rng.normal(size=(N, K)) / np.sqrt(K)).astype(np.float32)
+    b = rng.normal(size=N).astype(np.float32)
+    want = x.astype(np.float64) @ w.T.astype(np.float64) + b
+    if act == 1:
+        want = np.maximum(want, 0)
+    xd, wd, bd = (torch.from_numpy(a).cuda() for a in (x, w, b))
+    base = torch.full((M, N + 3), 7.0, device="cuda")
+    out = base[:, :N]
+    kernels.linear_into(out, xd, wd, bd, act, precision=_lib.PREC_3XTF32)
+    got = out.cpu().numpy()
+    assert rel_l2(got, want) <= 5e-6, rel_l2(got, want)
+    assert torch.all(base[:, N:] == 7.0)
+    i = M // 2
+    one = torch.empty((1, N), device="cuda")
+    kernels.linear_into(one, xd[i:i + 1], wd, bd, act, precision=_lib.PREC_3XTF32)
+    assert one.cpu().numpy().tobytes() == got[i:i + 1].tobytes()
+    _lib.call("glint_set_tuning", 9, 1)          # the v2 kernel
+    try:
+        ref = torch.empty((M, N), device="cuda")
+        kernels.linear_into(ref, xd, wd, bd, act, precision=_lib.PREC_3XTF32)
+    finally:
+        _lib.call("glint_set_tuning", 9, 0)
+    assert rel_l2(got, ref.cpu().numpy()) <= 2e-6
+
+
+@pytest.mark.parametrize("M,heads,dh,K", [(1000, 4, 64, 100), (777, 4, 47, 256), (300, 2, 32, 64),
+                                          (5, 8, 8, 16)])
+def test_tcgen05_v3_gat_project(cuda, M, heads, dh, K):
+    """Fused projection + score epilogue on the v3 kernel vs fp64 (Z and s_src/s_dst)."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(M + heads * dh + K)
+    x = rng.normal(size=(M, K)).astype(np.float32)
+    w = (rng.normal(size=(heads, dh, K)) / np.sqrt(K)).astype(np.float32)
+    att = rng.normal(size=(heads, 2 * dh)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    w_pad = kernels.padded_head_weight(torch.from_numpy(w).cuda())
+    Z, ss, sd = kernels.attn_project(xd, w_pad, torch.from_numpy(att).cuda(), heads, dh,
+                                     precision=_lib.PREC_3XTF32)
+    hp = kernels.head_pitch(dh)
+    z = Z.cpu().numpy().reshape(M, heads, hp)[:, :, :dh]
+    want = np.einsum("mk,hdk->mhd", x.astype(np.float64), w.astype(np.float64))
+    assert rel_l2(z, want) <= 5e-6
+    ws = np.einsum("mhd,hd->mh", want, att[:, :dh].astype(np.float64))
+    wdst = np.einsum("mhd,hd->mh", want, att[:, dh:].astype(np.float64))
+    assert rel_l2(ss.cpu().numpy(), ws) <= 1e-5
+    assert rel_l2(sd.cpu().numpy(), wdst) <= 1e-5
+
+
 def test_shape_errors_are_value_errors(cuda):
     from paper_2211_15082_b200 import kernels
 
