@@ -95,6 +95,10 @@ int glint_abi_version(void);
                                      shape allows, 1 the v2 kernel */
 #define GLINT_TUNE_GEMM_PF 10    /* v3 K2: L2 prefetch of A, tiles ahead (0 default = 1,
                                      -1 off) */
+#define GLINT_TUNE_L2_HINT 11    /* K1 regular rows: L2 policy per gathered row from the
+                                     hot bit of its id (glint_hot_annotate): 0 none,
+                                     1 hot evict_last + cold evict_first, 2 hot
+                                     evict_last only, 3 all evict_first */
 #define GLINT_TUNE_COUNT 12
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);

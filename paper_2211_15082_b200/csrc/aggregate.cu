@@ -48,11 +48,15 @@ struct RowAddr {
   __device__ __forceinline__ int64_t csr_row(int64_t r) const {
     return row_ids ? row_ids[r] : row_base + r;
   }
+  // Source ids are < 2^31; bit 31 of a stored id may carry the L2 "hot source"
+  // annotation (glint_hot_annotate), so every id is masked before use.
   __device__ __forceinline__ int64_t map(int64_t u) const {
+    u &= 0x7fffffff;
     return col_map ? static_cast<int64_t>(col_map[u]) : u;
   }
   // 32-bit form for the hot loops (ids and mapped rows are < 2^31)
   __device__ __forceinline__ int32_t map32(int32_t u) const {
+    u &= 0x7fffffff;
     return col_map ? __ldg(col_map + u) : u;
   }
   __device__ __forceinline__ int64_t self_row(int64_t r, int64_t rid) const {
@@ -86,6 +90,8 @@ struct MeanArgs {
   int64_t ld_out;
   const float* __restrict__ bias;  // optional epilogue: act(mean + bias)
   int act;
+  int l2_hint;   // 0 none; 1 hot ids evict_last / others evict_first; 2 hot evict_last only;
+                 // 3 all evict_first (GLINT_TUNE_L2_HINT; results never change)
 };
 
 __device__ __forceinline__ float mean_epilogue(const MeanArgs& a, float v, int col) {
@@ -534,6 +540,25 @@ int launch_hub(const MeanArgs& a, cudaStream_t s) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+               ::"r"(dst), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -551,7 +576,9 @@ __device__ __forceinline__ const float* row_at(const char* base, int32_t u, int3
 }
 
 // MAP = false: no column map (full mode), so the per-edge id needs no lookup.
-template <int LPR, int VPL, int R, int STRIDE = kThreads, int B = 1, bool MAP = true>
+// HINT: per-edge L2 policy from the id's hot bit (MeanArgs::l2_hint).
+template <int LPR, int VPL, int R, int STRIDE = kThreads, int B = 1, bool MAP = true,
+          bool HINT = false>
 __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int lane_g,
                                                unsigned gmask, float4* ring, int col0 = 0) {
   // ring: this lane's slots, slot (t, k) at ring[(t * VPL + k) * STRIDE]; the
@@ -568,6 +595,11 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
 
   const char* hbase = reinterpret_cast<const char*>(a.h + col0 + lane_g * 4);
   const int32_t ldb = static_cast<int32_t>(a.ld_h * 4);
+  uint64_t pol_hot = 0, pol_cold = 0;
+  if constexpr (HINT) {
+    pol_hot = a.l2_hint == 3 ? policy_evict_first() : policy_evict_last();
+    pol_cold = a.l2_hint == 2 ? policy_evict_normal() : policy_evict_first();
+  }
   // issue cursor: edge `ie`, index chunk [cb, cb+LPR) held in `cur`, next in `nxt`
   int ie = 0, cb = 0;
   int32_t cur = (lane_g < deg) ? __ldg(a.ra.indices + beg + lane_g) : 0;
@@ -579,12 +611,21 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
     }
     const int32_t id = __shfl_sync(gmask, cur, ie - cb, LPR);
-    const float* src = row_at(hbase, MAP ? a.ra.map32(id) : id, ldb);
+    const float* src = row_at(hbase, MAP ? a.ra.map32(id) : (id & 0x7fffffff), ldb);
+    if constexpr (HINT) {
+      const uint64_t pol = id < 0 ? pol_hot : pol_cold;
 #pragma unroll
-    for (int k = 0; k < VPL; ++k)
-      if (ok[k])
-        cp_async16(ring_s + static_cast<uint32_t>((slot * VPL + k) * STRIDE) * 16u,
-                   src + LPR * 4 * k);
+      for (int k = 0; k < VPL; ++k)
+        if (ok[k])
+          cp_async16_hint(ring_s + static_cast<uint32_t>((slot * VPL + k) * STRIDE) * 16u,
+                          src + LPR * 4 * k, pol);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        if (ok[k])
+          cp_async16(ring_s + static_cast<uint32_t>((slot * VPL + k) * STRIDE) * 16u,
+                     src + LPR * 4 * k);
+    }
     ++ie;
   };
 
@@ -650,7 +691,7 @@ __device__ __forceinline__ void mean_row_async(const MeanArgs& a, int64_t r, int
   }
 }
 
-template <int LPR, int VPL, int R, int MINB, int B = 1, bool MAP = true>
+template <int LPR, int VPL, int R, int MINB, int B = 1, bool MAP = true, bool HINT = false>
 __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) {
   extern __shared__ __align__(16) float4 ring_all[];
   constexpr int G = 32 / LPR;
@@ -663,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, MINB) mean_async_kernel(MeanArgs a) 
   if (idx >= a.sc.n_rows) return;
   const int64_t r = a.sc.schedule ? static_cast<int64_t>(a.sc.schedule[idx]) : idx;
   const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (group * LPR));
-  mean_row_async<LPR, VPL, R, kThreads, B, MAP>(a, r, lane_g, gmask, ring_all + threadIdx.x);
+  mean_row_async<LPR, VPL, R, kThreads, B, MAP, HINT>(a, r, lane_g, gmask, ring_all + threadIdx.x);
 }
 
 // Hub rows, per-lane cp.async ring: one warp per (hub row, 128-column block),
@@ -711,6 +752,8 @@ int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GLINT_CUDA(cudaFuncSetAttribute(mean_async_kernel<LPR, VPL, R, MINB, B, false, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured.mark();
   }
   const int64_t grid = ceil_div(a.sc.n_rows - a.sc.n_hub, kWarps * G);
@@ -721,6 +764,9 @@ int launch_mean_async(const MeanArgs& a, cudaStream_t s) {
   }
   if (a.ra.col_map)
     mean_async_kernel<LPR, VPL, R, MINB, B, true><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
+  else if (a.l2_hint)
+    mean_async_kernel<LPR, VPL, R, MINB, B, false, true>
+        <<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   else
     mean_async_kernel<LPR, VPL, R, MINB, B, false><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   return launch_status("spmm_mean_async");
@@ -1957,6 +2003,7 @@ int glint_spmm_mean_f32(int64_t n_rows, int32_t dim, const int64_t* indptr,
   a.ld_out = ld_out;
   a.bias = bias;
   a.act = act;
+  a.l2_hint = tuning(GLINT_TUNE_L2_HINT);
   a.sc.schedule = schedule;
   a.sc.n_rows = n_rows;
   a.sc.n_hub = n_hub;

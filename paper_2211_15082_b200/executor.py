@@ -1317,8 +1317,9 @@ class _HostSink:
         return self.host.numpy()
 
 
-def _exchange_for(distributed, mode, g):
-    """RowExchange when running full-mode inference across torch.distributed ranks."""
+def _exchange_for(distributed, mode, g, kind="replicate"):
+    """RowExchange when running full-mode inference across torch.distributed ranks
+    (kind "halo": each rank receives only the rows its CSR slice reads)."""
     if distributed is False or mode != "full":
         return None
     import torch.distributed as dist
@@ -1327,17 +1328,21 @@ def _exchange_for(distributed, mode, g):
         if distributed is True:
             raise ConfigError("distributed=True needs an initialised process group")
         return None
-    from .parallel import RowExchange, edge_balanced_ranges
+    from .parallel import HaloPlan, RowExchange, edge_balanced_ranges
 
+    if kind not in ("replicate", "halo"):
+        raise ConfigError(f"unknown exchange {kind!r} (replicate | halo)")
     world = dist.get_world_size()
-    return RowExchange(edge_balanced_ranges(g.indptr_host, world), dist.get_rank(), world)
+    cuts = edge_balanced_ranges(g.indptr_host, world)
+    halo = HaloPlan(g.indptr_host, g.indices, cuts, dist.get_rank()) if kind == "halo" else None
+    return RowExchange(cuts, dist.get_rank(), world, halo=halo)
 
 
 def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanout=None, seed=0,
                   executor="layerwise", order="none", budget=None, thresholds=None,
                   batch_size=1024, store_backing="memory", workdir=None, output="auto",
                   precision=None, distributed="auto", reassociate=False,
-                  probe=None) -> InferenceResult:
+                  probe=None, exchange="replicate") -> InferenceResult:
     """End to end: reorder, annotate, execute, de-permute (glint/executor.py:481-543).
 
     ``budget`` may be a DeviceBudget (reference behaviour) or ``"device"``:
@@ -1349,6 +1354,10 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     an initialised torch.distributed group (one process per GPU, NCCL); each
     rank computes its edge-balanced node range and returns the full output.
     Batch records / stats then describe the calling rank's own batches.
+    ``exchange``: "replicate" broadcasts every rank's rows of each exchanged
+    layer to all ranks; "halo" ships each rank only the rows its CSR slice
+    reads (one all-to-all per layer; tools/halo_fraction.py measures the
+    saving).  Outputs are byte-identical either way.
     ``reassociate=True`` (opt-in) computes a width-narrowing ConvMean as
     mean(h W^T) + b: exact in real arithmetic, ~1e-7 apart in fp32, and it
     gathers d_out instead of d_in floats per edge.  Off by default so that
@@ -1437,7 +1446,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     if executor == "layerwise":
         schedule = split(m)
         bud = resolve_budget(budget, _resident_bytes(m, schedule, tsets, g_i))
-        ex = _exchange_for(distributed, mode, g_i)
+        ex = _exchange_for(distributed, mode, g_i, exchange)
         eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision,
                               row_range=ex.row_range if ex else None, reassociate=reassociate)
         row_ids = tsets.v_sets[m.depth if m.depth else 0]
@@ -1456,7 +1465,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         eng.probe = probe
         store = eng.run(exchange=ex)
         if ex is not None:
-            ex.exchange_tensor(store.data)      # every rank returns the full output
+            ex.replicate_tensor(store.data)     # every rank returns the full output
         if streamed is None:
             wanted = user_targets if node_order.is_identity() else node_order.inv[user_targets]
             out_dev = _gather_rows(store, row_ids, wanted, dg0.device)

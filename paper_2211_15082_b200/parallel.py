@@ -15,8 +15,17 @@ Split points balance aggregation bytes, not node counts: the cost of a row is
 proportional to deg + 1 (its gathered rows), so p_k is the first node whose
 prefix of (deg + 1) reaches k/P of the total.
 
+Halo option (``kind="halo"``): a rank's aggregation reads only its own rows
+and the source rows its CSR slice references, so instead of replicating every
+slice everywhere each rank ships rank j exactly the rows of its range that j's
+slice reads -- one all-to-all (variable splits) per exchanged store.  Every
+rank holds the full CSR, so each computes every pair's row lists locally
+(HaloPlan, once per run).  Rows nobody references are never sent; their
+stale values are never read.  The model output is still replicated in full.
+Measured halo sizes on the cfg5 graph: tools/halo_fraction.py.
+
 Outputs are bit-identical for every P (tests/test_parallel_cpu.py checks the
-partition and exchange logic on gloo; the GPU engine is the same code path
+partition and both exchanges on gloo; the GPU engine is the same code path
 with a row range).
 """
 
@@ -40,6 +49,75 @@ def edge_balanced_ranges(indptr_host, parts) -> np.ndarray:
     return np.maximum.accumulate(np.minimum(cuts, n))
 
 
+class HaloPlan:
+    """Per-pair row lists of the halo exchange for `rank`.
+
+    recv[k]: ascending global ids in rank k's range that this rank's CSR slice
+    reads (received from k); send[j]: ids in this rank's range that rank j's
+    slice reads (sent to j).  Self entries are empty.  Built from the full CSR
+    (indptr on the host, indices on any device) with one unique() per slice."""
+
+    def __init__(self, indptr_host, indices, cuts, rank):
+        import torch
+
+        self.cuts = np.asarray(cuts, dtype=np.int64)
+        self.rank = int(rank)
+        world = len(self.cuts) - 1
+        indptr_host = np.asarray(indptr_host, dtype=np.int64)
+        dev = indices.device
+        need = []                     # need[j][k]: rows of k's range read by j's slice
+        for j in range(world):
+            lo, hi = int(self.cuts[j]), int(self.cuts[j + 1])
+            src = torch.unique(indices[int(indptr_host[lo]):int(indptr_host[hi])].to(torch.int64))
+            bounds = torch.searchsorted(src, torch.as_tensor(self.cuts, device=dev))
+            row = []
+            for k in range(world):
+                if k == j:
+                    row.append(src[:0])
+                else:
+                    row.append(src[int(bounds[k]):int(bounds[k + 1])])
+            need.append(row)
+        self.recv = [need[self.rank][k] for k in range(world)]
+        self.send = [need[j][self.rank] for j in range(world)]
+        self.recv_rows = torch.cat(self.recv) if world else indices.new_zeros(0, dtype=torch.int64)
+        self.send_rows = torch.cat(self.send) if world else indices.new_zeros(0, dtype=torch.int64)
+        self.recv_counts = [int(t.numel()) for t in self.recv]
+        self.send_counts = [int(t.numel()) for t in self.send]
+
+    def fraction(self, num_nodes):
+        """Rows received / rows a full replication would receive."""
+        own = int(self.cuts[self.rank + 1] - self.cuts[self.rank])
+        return sum(self.recv_counts) / max(1, int(num_nodes) - own)
+
+
+def _take_rows(data, rows):
+    """data[rows] into a dense buffer: the glint row-copy kernel on CUDA; host
+    tensors (the gloo logic tests) use torch indexing."""
+    import torch
+
+    out = torch.empty((rows.numel(), data.shape[1]), dtype=data.dtype, device=data.device)
+    if rows.numel() == 0:
+        return out
+    if data.is_cuda:
+        from . import kernels
+
+        kernels.copy_rows(out, data, src_rows=rows)
+    else:
+        out.copy_(data[rows])
+    return out
+
+
+def _put_rows(data, rows, buf):
+    if rows.numel() == 0:
+        return
+    if data.is_cuda:
+        from . import kernels
+
+        kernels.copy_rows(data, buf, dst_rows=rows)
+    else:
+        data[rows] = buf
+
+
 class RowExchange:
     """Broadcast each rank's slice of every store read later.
 
@@ -50,10 +128,13 @@ class RowExchange:
     -- on the collective stream, while the next batches compute.  The block
     end posts whatever is left and waits."""
 
-    def __init__(self, cuts, rank, world, group=None, chunks=4):
+    def __init__(self, cuts, rank, world, group=None, chunks=4, halo=None):
         self.cuts = np.asarray(cuts, dtype=np.int64)
         self.rank, self.world, self.group = int(rank), int(world), group
-        self.chunks = max(1, int(chunks))
+        self.halo = halo                # HaloPlan: ship only the rows other ranks read
+        # the halo exchange runs once per store at the block end (its rows are
+        # scattered, not contiguous pieces)
+        self.chunks = 1 if halo is not None else max(1, int(chunks))
         self.bytes_sent = 0
         self._blk = None
         self._posted = 0
@@ -106,7 +187,29 @@ class RowExchange:
                 dist.broadcast(t, src=k, group=self.group, async_op=True)
         return [cm]
 
+    def _halo_exchange(self, data):
+        """One all-to-all: this rank's rows that rank j reads go to j; the rows
+        this rank reads from rank k arrive from k and are scattered in place."""
+        import torch.distributed as dist
+
+        plan = self.halo
+        send = _take_rows(data, plan.send_rows)
+        recv = data.new_empty((plan.recv_rows.numel(), data.shape[1]))
+        self.bytes_sent += send.numel() * send.element_size()
+        dist.all_to_all_single(recv, send, output_split_sizes=plan.recv_counts,
+                               input_split_sizes=plan.send_counts, group=self.group)
+        _put_rows(data, plan.recv_rows, recv)
+
     def _post(self, engine, keys, upto):
+        if self.halo is not None:
+            if self._posted < upto:
+                for key in keys:
+                    data = engine.stores[key].data
+                    # the store may be wider than its pitch view: exchange the
+                    # underlying row-major rows
+                    self._halo_exchange(data)
+                self._posted = upto
+            return
         while self._posted < upto:
             c = self._posted
             parts = []
@@ -149,7 +252,19 @@ class RowExchange:
         self.exchange_tensors((data,))
 
     def exchange_tensors(self, tensors):
-        """exchange_tensor over several row-aligned tensors in one grouped collective."""
+        """exchange_tensor over several row-aligned tensors in one grouped
+        collective (halo mode: only the rows other ranks' slices read)."""
+        if self.halo is not None:
+            for data in tensors:
+                self._halo_exchange(data)
+            return
+        self.replicate_tensors(tensors)
+
+    def replicate_tensor(self, data):
+        """Every rank gets every row (the model output), whatever the mode."""
+        self.replicate_tensors((data,))
+
+    def replicate_tensors(self, tensors):
         parts = []
         for k in range(self.world):
             lo, hi = int(self.cuts[k]), int(self.cuts[k + 1])

@@ -41,13 +41,15 @@ def main():
     def check(tag, m, hg, xx, cap, reassoc):
         kw = dict(budget=DeviceBudget(cap), reassociate=reassoc)
         ref = run_inference(m, hg, xx, distributed=False, **kw).output
-        out = run_inference(m, hg, xx, distributed="auto", **kw).output
-        flags = torch.tensor([1.0 if np.array_equal(ref, out) else 0.0], device="cuda")
-        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
-        if rank == 0:
-            print(json.dumps({"graph": tag, "model": name, "world": world, "nodes": hg.num_nodes,
-                              "capacity": cap, "reassociate": reassoc,
-                              "bit_identical_all_ranks": bool(flags.item() == 1.0)}), flush=True)
+        for kind in ("replicate", "halo"):
+            out = run_inference(m, hg, xx, distributed="auto", exchange=kind, **kw).output
+            flags = torch.tensor([1.0 if np.array_equal(ref, out) else 0.0], device="cuda")
+            dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+            if rank == 0:
+                print(json.dumps({"graph": tag, "model": name, "world": world,
+                                  "nodes": hg.num_nodes, "capacity": cap, "reassociate": reassoc,
+                                  "exchange": kind,
+                                  "bit_identical_all_ranks": bool(flags.item() == 1.0)}), flush=True)
 
     for name, m in models:
         for cap in (1 << 34, 64 << 20):       # one batch per layer / many batches
