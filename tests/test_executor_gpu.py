@@ -231,7 +231,8 @@ def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
         assert out.returncode == 0, out.stderr[-2000:]
         lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
         runs = [x for x in lines if "model" in x]
-        assert len(runs) == 6 + 3, lines
+        assert len(runs) == 2 * (6 + 3), lines        # replicate and halo exchange
+        assert {x["exchange"] for x in runs} == {"replicate", "halo"}
         assert all(x["bit_identical_all_ranks"] for x in runs), runs
         star = next(x for x in lines if "star_cuts" in x)
         assert star["empty_ranks"] >= (world > 2)      # a rank without rows took part
