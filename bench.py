@@ -455,20 +455,33 @@ def roofline(summ, agg_name, steps, ms):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    cnt, nbytes, agg_ms = summ.get(agg_name, (0, 0, 0.0))
+    # aggregation launches: K1 (spmm_mean) or K4 (gat_aggregate), plus K7
+    # (conv_mean: an aggregate-first ConvMean's aggregation fused with its
+    # transform; its bytes are B_agg plus the output rows)
+    names = [agg_name] + (["conv_mean"] if agg_name == "spmm_mean" else [])
+    per = {nm: summ[nm] for nm in names if nm in summ}
+    cnt = sum(v[0] for v in per.values())
+    nbytes = sum(v[1] for v in per.values())
+    agg_ms = sum(v[2] for v in per.values())
     achieved = (nbytes / (agg_ms / 1e3) / 1e9) if agg_ms else None
     lin = summ.get("linear", (0, 0, 0.0))
     k = max(steps, 1)
     return {
-        "kernel": agg_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+        "kernel": "+".join(per) or agg_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+        "per_kernel": {nm: {"launches_per_step": v[0] // k, "bytes_per_step": v[1] // k,
+                            "ms_per_step": v[2] / k,
+                            "gbs": (v[1] / (v[2] / 1e3) / 1e9) if v[2] else None}
+                       for nm, v in per.items()},
         "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
         "traffic": traffic_from_profiles(agg_name),
+        "traffic_kernel": agg_name,
         "traffic_basis": "DRAM read+write bytes per aggregation launch (regular + hub kernels), "
                          "ncu launch list of this bench step (profiles/ncu_traffic.json); "
                          "compare with algorithmic_bytes_per_launch",
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-        "achieved_basis": "sum of SURVEY 8d B_agg over the step's aggregation launches / sum of "
-                          "their CUDA-event durations (same stream)",
+        "achieved_basis": "sum of SURVEY 8d B_agg over the step's aggregation launches (K7: "
+                          "B_agg + its output rows) / sum of their CUDA-event durations "
+                          "(same stream)",
         "launches_per_step": cnt // k,
         "algorithmic_bytes_per_launch": nbytes // max(cnt, 1),
         "algorithmic_bytes_per_step": nbytes // k,

@@ -99,11 +99,15 @@ int glint_abi_version(void);
                                      hot bit of its id (glint_hot_annotate): 0 none,
                                      1 hot evict_last + cold evict_first, 2 hot
                                      evict_last only, 3 all evict_first */
-#define GLINT_TUNE_COUNT 12
+#define GLINT_TUNE_FUSED_VARIANT 12 /* K7 gather warps x ring depth: 0 26x8 (26x6,
+                                       16x8 when shared memory is short), 1 24x8,
+                                       2 20x10, 3 16x12 */
+#define GLINT_TUNE_FUSED_PROF 13  /* K7: 1 phase-cycle counters (glint_debug_counters 1) */
+#define GLINT_TUNE_COUNT 14
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of
- * kernel family `which` (0 = tcgen05 GEMM). */
+ * kernel family `which` (0 = tcgen05 GEMM, 1 = K7 fused conv). */
 int glint_debug_counters(int which, uint64_t* host_out, int n, int reset);
 /* host pointers; fills the properties of `device` */
 int glint_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
@@ -160,6 +164,34 @@ int glint_linear_f32(int64_t M, int32_t N, int32_t K, const float* A,
                      int64_t lda, const int64_t* a_rows, const float* W,
                      int64_t ldw, const float* bias, int32_t act, float* C,
                      int64_t ldc, int32_t precision, glint_stream_t stream);
+
+/* ----------------------------------------- K7 fused aggregate -> transform
+ * Replaces model_ir.py:336-338 (ConvMean: agg_mean kernels.py:122-135, then
+ * linear kernels.py:95-107) for an aggregate-first layer in ONE kernel:
+ *   out[r, n] = act( sum_k mean_r[k] * W[n, k] + bias[n] )
+ * where mean_r is exactly glint_spmm_mean_f32's row r (same add chain, same
+ * division; row addressing, self_rows and col_map as there) and the transform
+ * is glint_linear_f32's 3xTF32 product order.  The B x dim_in aggregate
+ * never reaches HBM.  `schedule` (nullable) is glint_degree_schedule's order
+ * over all n_rows rows (no hub split: rows are taken dynamically by warps).
+ * Shapes: glint_conv_mean_supported(dim_in, dim_out) (dim_in <= 128, a
+ * multiple of 4, dim_out <= 256); ld_h, ld_out multiples of 4 with 16-byte
+ * aligned h / out; otherwise GLINT_EUNSUPPORTED (the caller runs K1 + K2).
+ * max_ctas > 0 caps the persistent grid (default 0: one CTA per SM, each
+ * holding a whole SM): leaving a few SMs free lets concurrent work on other
+ * streams (the batch planner's counting kernels) run beside it.
+ * Workspace: glint_conv_mean_workspace_bytes (the pre-split W panel and a
+ * tile counter). */
+size_t glint_conv_mean_workspace_bytes(int32_t dim_in, int32_t dim_out);
+int glint_conv_mean_supported(int32_t dim_in, int32_t dim_out);
+int glint_conv_mean_f32(int64_t n_rows, int32_t dim_in, int32_t dim_out,
+                        const int64_t* indptr, const int32_t* indices,
+                        const int64_t* row_ids, int64_t row_base,
+                        const int64_t* self_rows, const int32_t* col_map,
+                        const float* h, int64_t ld_h, const float* W, int64_t ldw,
+                        const float* bias, int32_t act, float* out, int64_t ld_out,
+                        const int32_t* schedule, int32_t max_ctas, void* workspace,
+                        size_t workspace_bytes, glint_stream_t stream);
 
 /* -------------------------------------------------------- K3/K4 attention
  * Replaces kernels.py:170-203 agg_attn.  The projection z_h = linear(h, W_h)

@@ -46,6 +46,10 @@ SIGNATURES = {
     "glint_device_info": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P]),
     "glint_spmm_mean_f32": (ctypes.c_int, [_I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _I64,
                                            _P, _I64, _P, _I64, _P, _I32, _P]),
+    "glint_conv_mean_workspace_bytes": (_SZ, [_I32, _I32]),
+    "glint_conv_mean_supported": (ctypes.c_int, [_I32, _I32]),
+    "glint_conv_mean_f32": (ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _I64, _P, _P, _P, _I64,
+                                           _P, _I64, _P, _I32, _P, _I64, _P, _I32, _P, _SZ, _P]),
     "glint_degree_schedule_workspace_bytes": (_SZ, []),
     "glint_degree_schedule": (ctypes.c_int, [_I64, _P, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "glint_linear_f32": (ctypes.c_int, [_I64, _I32, _I32, _P, _I64, _P, _P, _I64, _P, _I32,
@@ -122,7 +126,7 @@ def last_error() -> str:
 
 # Kernels launched per call (for the bench's launch count); host-only or
 # memset-only entry points launch none.
-KERNELS_PER_CALL = {"glint_degree_schedule": 3, "glint_idset_finalize": 4,
+KERNELS_PER_CALL = {"glint_conv_mean_f32": 2, "glint_degree_schedule": 3, "glint_idset_finalize": 4,
                     "glint_degree_prefix": 3, "glint_hub_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
                     "glint_rcmk_sorted_host": 0, "glint_sample_neighbors": 4,
                     "glint_gat_aggregate_ws_f32": 2, "glint_upload_start": 0, "glint_upload_start_packed": 1, "glint_copy_rows_async": 0,

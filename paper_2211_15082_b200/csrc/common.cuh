@@ -30,6 +30,8 @@ int sm_count();  // cached per current device
 
 int tuning(int key);  // glint_set_tuning knobs (0 = default behaviour)
 
+int fused_debug_counters(uint64_t* host_out, int n, int reset);   // K7 phase counters
+
 constexpr int kWarp = 32;
 
 // Once-per-device guard for host-side kernel configuration

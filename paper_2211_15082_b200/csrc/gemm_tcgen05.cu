@@ -1806,8 +1806,9 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
 }  // namespace glint
 
 extern "C" int glint_debug_counters(int which, uint64_t* host_out, int n, int reset) {
-  GLINT_REQUIRE(which == 0 && n >= 0 && n <= 8 && (host_out || n == 0),
+  GLINT_REQUIRE((which == 0 || which == 1) && n >= 0 && n <= 8 && (host_out || n == 0),
                 "debug_counters: bad argument");
+  if (which == 1) return glint::fused_debug_counters(host_out, n, reset);
   if (n) GLINT_CUDA(cudaMemcpyFromSymbol(host_out, glint::g_gemm_prof, n * sizeof(uint64_t)));
   if (reset) {
     const unsigned long long zeros[8] = {0};

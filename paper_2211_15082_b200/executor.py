@@ -28,13 +28,14 @@ are computed on the host as in the reference and uploaded.
 from __future__ import annotations
 
 import os
+import sys
 import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib, device as devmodel, kernels
-from .batching import BatchController, Thresholds
+from .batching import BatchController, Thresholds, next_batch
 from .errors import ConfigError, DeviceAllocationError, DeviceCapacityError, InternalError
 from .model_ir import ModelGraph
 from .reorder import NodeOrder, apply_order_device, make_order
@@ -415,6 +416,8 @@ class LayerwiseEngine:
         self.sink_chunks = int(os.environ.get("GLINT_SINK_CHUNKS", "2"))
         # one launch per full-mode conv layer when the budget admits it
         self.whole_layer = os.environ.get("GLINT_WHOLE_LAYER", "1") == "1"
+        self._fused_ctas = 0            # K7 grid cap while planning runs beside it
+        self._fused_ok = True           # K7 allowed for the launch in progress
 
     # -- helpers ------------------------------------------------------------
 
@@ -488,6 +491,11 @@ class LayerwiseEngine:
             elif full and n_t == n_nodes:
                 n_i = n_t
                 n_h = int(hub_host[n_nodes])
+            elif full and (start, end) in gl._cache.get("plan_counts", {}):
+                # full-mode counts are a pure function of the (immutable) graph
+                # and the contiguous range: memoized on the DeviceGraph, so a
+                # repeated run plans the same batches without counting kernels
+                n_i, n_h = gl._cache["plan_counts"][(start, end)]
             else:
                 ids = gl._cache.get("plan_idset")      # reused across batches and runs
                 gl.wait_rows(end if full else None, stream=self.plan_stream)
@@ -506,6 +514,11 @@ class LayerwiseEngine:
                     counts = torch.stack([ids.count_dev[0],
                                           hub_pre[end] - hub_pre[start]]).cpu()
                     n_i, n_h = int(counts[0]), int(counts[1])
+                if full:
+                    memo = gl._cache.setdefault("plan_counts", {})
+                    if len(memo) > 4096:
+                        memo.clear()
+                    memo[(start, end)] = (n_i, n_h)
             fp = devmodel.footprint_counts(blk, n_t, n_i, n_e, dims)
             return _Plan(start, end, n_i, n_e, n_h), fp
 
@@ -641,7 +654,7 @@ class LayerwiseEngine:
         sink_store = (self.stores.get(out_key) if self.sink is not None
                       and blk.block_id == self.schedule.model_output.block else None)
 
-        def run_rows(r0, r1, n_inputs):
+        def run_rows(r0, r1, n_inputs, whole=False):
             # Rows [r0, r1) may run as row chunks -- the kernels are row-invariant,
             # so the bytes are identical -- (a) in the final block, so each
             # finished chunk's device->host copy overlaps the next chunk, and (b)
@@ -671,6 +684,11 @@ class LayerwiseEngine:
                 c0, c1 = cuts[k], cuts[k + 1]
                 n_hub = int(hubs[k + 1] - hubs[k]) if hubs is not None else self._batch_hubs
                 sub = _Plan(c0, c1, n_inputs, int(prefix[c1] - prefix[c0]), n_hub)
+                # K7 walks a hub row with one warp: fine inside a whole-layer
+                # launch (the longest rows start first, other SMs keep going),
+                # but a row chunk or a batch would wait for its longest hub
+                # row, which K1's hub CTAs stream ~4x faster
+                self._fused_ok = (whole and len(cuts) == 2) or n_hub == 0
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
                                 gat_cache)
                 if self.probe is not None:
@@ -702,11 +720,21 @@ class LayerwiseEngine:
                                           self.dims), self.budget)):
             if self.probe is not None:
                 self.probe.mark(f"L{layer} whole layer [{lo},{hi})")
+            # The controller's batches after this launch need counting kernels
+            # (plan stream) unless its first batch is the whole range: K7's
+            # persistent grid then leaves SMs for them, so planning overlaps
+            # the layer instead of following it.
+            first_end = min(next_batch(prefix, lo, self.controller.thresholds), hi)
+            counts = ((first_end < hi or (hi - lo) < n_nodes)
+                      and (lo, first_end) not in gl._cache.get("plan_counts", {}))
+            self._fused_ctas = kernels.fused_ctas_beside_planning() if counts else 0
             try:
-                run_rows(lo, hi, n_nodes)
+                run_rows(lo, hi, n_nodes, whole=True)
                 spec["hi"] = hi
                 speculate = True
+                self._fused_ctas = 0
             except torch.cuda.OutOfMemoryError:
+                self._fused_ctas = 0
                 # the real allocator disagrees with the footprint model: fall
                 # back to the controller's batches (rows done so far are valid
                 # and are recomputed with the same bytes)
@@ -803,6 +831,8 @@ class LayerwiseEngine:
 
         sched = self._schedule(gl, row_ids, row_base, B, full) if blk.has_conv else None
         n_hub = plan.num_hubs
+        if self.probe is not None:
+            self.probe.mark(f"L{blk.layer} [{s},{e}) schedule")
 
         skip = set(fused.values())
         for o in blk.op_ids:
@@ -828,6 +858,31 @@ class LayerwiseEngine:
                 if self.probe is not None:
                     self.probe.end(agg_bytes(pitch_of(d_out), plan.num_edges, B))
                 self.kernel_launches += 1
+                mats[target] = out
+                if act_op is None:
+                    mats[o] = out
+            elif op.kind == "ConvMean" and self._fused_ok and kernels.conv_mean_supported(
+                    conv_source(op.inputs[0])[0], m.out_dims[o], self.precision):
+                # K7: aggregate and transform in one kernel; the B x d_in
+                # aggregate stays on chip (model_ir.py:336-338)
+                h, cmap = conv_source(op.inputs[0])
+                d_in, d_out = int(h.shape[1]), m.out_dims[o]
+                act_op = fused.get(o)
+                target = act_op or o
+                out = dest(target, d_out)
+                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
+                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                if self.probe is not None:
+                    self.probe.begin("conv_mean")
+                if os.environ.get("GLINT_DEBUG_FUSED"):
+                    print(f"conv_mean L{blk.layer} [{s},{e}) max_ctas={self._fused_ctas}",
+                          file=sys.stderr, flush=True)
+                kernels.conv_mean(out, h, self.params.w[o], self.params.b[o], act, gl.indptr,
+                                  gl.indices, B, row_ids=row_ids, row_base=row_base,
+                                  col_map=cmap, schedule=sched, max_ctas=self._fused_ctas)
+                if self.probe is not None:
+                    self.probe.end(conv_bytes(d_in, d_out, plan.num_edges, B))
+                self.kernel_launches += 2
                 mats[target] = out
                 if act_op is None:
                     mats[o] = out
@@ -1006,6 +1061,13 @@ def agg_bytes(width, n_edges, n_rows, heads=0) -> int:
     if heads:
         b += 4 * heads * (n_edges + 2 * n_rows)
     return b
+
+
+def conv_bytes(d_in, d_out, n_edges, n_rows) -> int:
+    """Algorithmic HBM bytes of one fused aggregate->transform launch (K7): the
+    aggregation's B_agg at d_in plus the d_out-wide output rows (the aggregate
+    itself never leaves the SM; W is L2-resident)."""
+    return agg_bytes(d_in, n_edges, n_rows) + 4 * pitch_of(d_out) * n_rows
 
 
 class KernelProbe:

@@ -22,6 +22,8 @@ numpy's einsum; they agree within the stated tolerance (tests use rel-L2 <=
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -41,6 +43,8 @@ HUB_MIN_DEGREE = 512
 # tcgen05 tensor cores (~1e-6 rel-L2 vs fp64); PREC_FP32 selects the CUDA-core
 # fp32 FMA-chain kernel.
 PRECISION = _lib.PREC_3XTF32
+# K7 fused aggregate->transform for aggregate-first ConvMeans (GLINT_FUSE_CONV=0: K1 + K2)
+FUSE_CONV = os.environ.get("GLINT_FUSE_CONV", "1") == "1"
 
 
 def _torch():
@@ -388,6 +392,47 @@ def spmm_mean(out, h, indptr, indices, n_rows, row_ids=None, row_base=0, self_ro
     _lib.call("glint_spmm_mean_f32", int(n_rows), dim, ptr(indptr), ptr(indices), ptr(row_ids),
               int(row_base), ptr(self_rows), ptr(col_map), ptr(h), ld(h), ptr(out), ld(out),
               ptr(schedule), int(n_hub), ptr(bias), int(act), stream_handle())
+    return out
+
+
+_SMS = {}
+
+
+def fused_ctas_beside_planning() -> int:
+    """K7 grid while the batch planner's counting kernels run beside it: all SMs
+    but GLINT_FUSED_RESERVE_SMS (default 8).  K7 holds a whole SM per CTA, so
+    without a reserve the planner's kernels wait for it to finish."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _SMS:
+        _SMS[dev] = torch.cuda.get_device_properties(dev).multi_processor_count
+    reserve = int(os.environ.get("GLINT_FUSED_RESERVE_SMS", "8"))
+    return max(1, _SMS[dev] - reserve) if reserve > 0 else 0
+
+
+def conv_mean_supported(h, d_out, precision=None) -> bool:
+    """Whether K7 (the fused aggregate->transform) takes this ConvMean: 3xTF32,
+    d_in <= 128 on a 16-byte row pitch, d_out <= 256."""
+    prec = PRECISION if precision is None else precision
+    d_in = int(h.shape[1])
+    return (prec == _lib.PREC_3XTF32 and FUSE_CONV and bool(_lib.query(
+        "glint_conv_mean_supported", d_in, int(d_out))) and ld(h) % 4 == 0
+        and ptr(h) % 16 == 0)
+
+
+def conv_mean(out, h, weight, bias, act, indptr, indices, n_rows, row_ids=None, row_base=0,
+              self_rows=None, col_map=None, schedule=None, max_ctas=0):
+    """K7 launch: out = act(mean(h) W^T + b) in one kernel (glint_conv_mean_f32),
+    the composition of spmm_mean and linear_into without the B x d_in aggregate
+    in HBM (model_ir.py:336-338)."""
+    torch = _torch()
+    d_in, d_out = int(h.shape[1]), int(out.shape[1])
+    nbytes = int(_lib.query("glint_conv_mean_workspace_bytes", d_in, d_out))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
+    _lib.call("glint_conv_mean_f32", int(n_rows), d_in, d_out, ptr(indptr), ptr(indices),
+              ptr(row_ids), int(row_base), ptr(self_rows), ptr(col_map), ptr(h), ld(h),
+              ptr(weight), ld(weight), ptr(bias), int(act), ptr(out), ld(out), ptr(schedule),
+              int(max_ctas), ptr(ws), nbytes, stream_handle())
     return out
 
 

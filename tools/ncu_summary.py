@@ -140,7 +140,8 @@ def main():
 
 # K1 / K4 calls: the regular-row kernel plus its concurrent hub-row kernel
 FAMILIES = {"spmm_mean": ("mean_async_kernel", "mean_kernel<", "mean_hub"),
-            "gat_aggregate": ("gat_kernel<", "gat_async_kernel", "gat_hub")}
+            "gat_aggregate": ("gat_kernel<", "gat_async_kernel", "gat_hub"),
+            "conv_mean": ("conv_mean_fused_kernel",)}
 
 
 def step_traffic(lfile):
