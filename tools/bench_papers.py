@@ -88,7 +88,8 @@ def main():
         del out, eng
         torch.cuda.empty_cache()
     ms = float(np.mean([st["ms"] for st in steps]))
-    cnt, nbytes, agg_ms = summ.get("spmm_mean", (0, 0, 0.0))
+    per = [summ.get(k, (0, 0, 0.0)) for k in ("spmm_mean", "conv_mean")]
+    cnt, nbytes, agg_ms = (sum(v[i] for v in per) for i in range(3))
     lin = summ.get("linear", (0, 0, 0.0))
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -99,7 +100,8 @@ def main():
         "nodes": n, "in_edges": g.num_edges, "graph_gen_s": round(gen_s, 1),
         "value": n / (ms / 1e3), "unit": "nodes/s", "ms_per_step": ms, "steps": args.steps,
         "warmup": args.warmup,
-        "aggregation": {"launches": cnt, "algorithmic_bytes": nbytes, "ms": agg_ms,
+        "aggregation": {"kernels": {k: v for k, v in summ.items() if k != "linear"},
+                        "launches": cnt, "algorithmic_bytes": nbytes, "ms": agg_ms,
                         "achieved_gbs": nbytes / (agg_ms / 1e3) / 1e9 if agg_ms else None,
                         "frac_of_peak": (nbytes / (agg_ms / 1e3) / 1e9 / peak) if agg_ms else None,
                         "peak_gbs": peak},
