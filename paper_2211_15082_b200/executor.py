@@ -342,6 +342,20 @@ def _plan_stream(device):
     return s
 
 
+_HUB_STREAMS: dict = {}
+
+
+def _hub_stream(device):
+    """High-priority side stream for the hub rows beside a K7 launch: its CTAs
+    take the SMs K7 leaves free as soon as they are issued."""
+    import torch
+
+    s = _HUB_STREAMS.get(device)
+    if s is None:
+        s = _HUB_STREAMS[device] = torch.cuda.Stream(device=device, priority=-1)
+    return s
+
+
 def _device_params(m: ModelGraph, device):
     """Device weights of a model, uploaded once per (model, device) and kept
     while the model object is alive (the model is immutable)."""
@@ -418,6 +432,7 @@ class LayerwiseEngine:
         self.whole_layer = os.environ.get("GLINT_WHOLE_LAYER", "1") == "1"
         self._fused_ctas = 0            # K7 grid cap while planning runs beside it
         self._fused_ok = True           # K7 allowed for the launch in progress
+        self.k7_launches = {"whole": 0, "split": 0}
 
     # -- helpers ------------------------------------------------------------
 
@@ -861,8 +876,9 @@ class LayerwiseEngine:
                 mats[target] = out
                 if act_op is None:
                     mats[o] = out
-            elif op.kind == "ConvMean" and self._fused_ok and kernels.conv_mean_supported(
-                    conv_source(op.inputs[0])[0], m.out_dims[o], self.precision):
+            elif op.kind == "ConvMean" and kernels.conv_mean_supported(
+                    conv_source(op.inputs[0])[0], m.out_dims[o], self.precision) and (
+                    self._fused_ok or (sched is not None and 0 < n_hub < B)):
                 # K7: aggregate and transform in one kernel; the B x d_in
                 # aggregate stays on chip (model_ir.py:336-338)
                 h, cmap = conv_source(op.inputs[0])
@@ -874,15 +890,21 @@ class LayerwiseEngine:
                        "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
                 if self.probe is not None:
                     self.probe.begin("conv_mean")
+                split = not self._fused_ok
                 if os.environ.get("GLINT_DEBUG_FUSED"):
-                    print(f"conv_mean L{blk.layer} [{s},{e}) max_ctas={self._fused_ctas}",
-                          file=sys.stderr, flush=True)
-                kernels.conv_mean(out, h, self.params.w[o], self.params.b[o], act, gl.indptr,
-                                  gl.indices, B, row_ids=row_ids, row_base=row_base,
-                                  col_map=cmap, schedule=sched, max_ctas=self._fused_ctas)
+                    print(f"conv_mean L{blk.layer} [{s},{e}) max_ctas={self._fused_ctas} "
+                          f"split_hubs={n_hub if split else 0}", file=sys.stderr, flush=True)
+                if split:
+                    self._hub_rows_beside_k7(out, h, cmap, o, act, gl, row_ids, row_base, sched,
+                                             n_hub, B)
+                else:
+                    kernels.conv_mean(out, h, self.params.w[o], self.params.b[o], act, gl.indptr,
+                                      gl.indices, B, row_ids=row_ids, row_base=row_base,
+                                      col_map=cmap, schedule=sched, max_ctas=self._fused_ctas)
+                self.k7_launches["split" if split else "whole"] += 1
                 if self.probe is not None:
                     self.probe.end(conv_bytes(d_in, d_out, plan.num_edges, B))
-                self.kernel_launches += 2
+                self.kernel_launches += 5 if split else 2
                 mats[target] = out
                 if act_op is None:
                     mats[o] = out
@@ -955,6 +977,42 @@ class LayerwiseEngine:
                 if mat.data_ptr() != view.data_ptr():
                     kernels.copy_rows(view, mat)
                     self.kernel_launches += 1
+
+    def _hub_rows_beside_k7(self, out, h, cmap, o, act, gl, row_ids, row_base, sched, n_hub, B):
+        """K7 over a launch whose schedule starts with hub rows (a row chunk or a
+        batch): the regular rows [n_hub, B) of the schedule run as K7 on all
+        but `GLINT_FUSED_RESERVE_SMS` SMs, while the hub rows run beside it on a
+        high-priority side stream as K1's hub CTAs into a compact buffer, K2,
+        and a row scatter into `out`.  K7 would walk a hub row with one warp,
+        and the launch would wait for its longest hub row.  Same bytes as K7 or
+        K1 + K2 (row invariance)."""
+        import torch
+
+        main = torch.cuda.current_stream(self.dev)
+        side = _hub_stream(self.dev)
+        side.wait_stream(main)
+        sched.record_stream(side)
+        if row_ids is not None:
+            row_ids.record_stream(side)
+        d_in, d_out = int(h.shape[1]), int(out.shape[1])
+        with torch.cuda.stream(side):
+            hub_pos = sched[:n_hub].to(torch.int64)
+            csr_rows = (hub_pos + row_base) if row_ids is None else row_ids[hub_pos]
+            agg = torch.empty((n_hub, pitch_of(d_in)), dtype=torch.float32,
+                              device=self.dev)[:, :d_in]
+            all_hubs = torch.arange(n_hub, dtype=torch.int32, device=self.dev)
+            kernels.spmm_mean(agg, h, gl.indptr, gl.indices, n_hub, row_ids=csr_rows,
+                              col_map=cmap, schedule=all_hubs, n_hub=n_hub)
+            res = torch.empty((n_hub, pitch_of(d_out)), dtype=torch.float32,
+                              device=self.dev)[:, :d_out]
+            kernels.linear_into(res, agg, self.params.w[o], self.params.b[o], act,
+                                precision=self.precision)
+            kernels.copy_rows(out, res, dst_rows=hub_pos)
+        kernels.conv_mean(out, h, self.params.w[o], self.params.b[o], act, gl.indptr,
+                          gl.indices, B - n_hub, row_ids=row_ids, row_base=row_base,
+                          col_map=cmap, schedule=sched[n_hub:],
+                          max_ctas=kernels.fused_ctas_beside_planning())
+        main.wait_stream(side)
 
     def _transform(self, o, layer_mats, layer_spaces):
         """Per-layer source transform of a transform-first conv: z = h W^T for a
