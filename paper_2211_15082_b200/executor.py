@@ -433,6 +433,9 @@ class LayerwiseEngine:
         self._fused_ctas = 0            # K7 grid cap while planning runs beside it
         self._fused_ok = True           # K7 allowed for the launch in progress
         self.k7_launches = {"whole": 0, "split": 0}
+        # whole-layer K7 launches keep their hub rows inside (default) or run
+        # them beside K7 as in row chunks (GLINT_K7_HUBS=beside, A/B)
+        self.k7_hubs_beside = os.environ.get("GLINT_K7_HUBS", "inside") == "beside"
 
     # -- helpers ------------------------------------------------------------
 
@@ -703,7 +706,8 @@ class LayerwiseEngine:
                 # launch (the longest rows start first, other SMs keep going),
                 # but a row chunk or a batch would wait for its longest hub
                 # row, which K1's hub CTAs stream ~4x faster
-                self._fused_ok = (whole and len(cuts) == 2) or n_hub == 0
+                self._fused_ok = ((whole and len(cuts) == 2 and not self.k7_hubs_beside)
+                                  or n_hub == 0)
                 self._run_batch(blk, gl, sub, full, targets_dev, layer_mats, layer_spaces, fused,
                                 gat_cache)
                 if self.probe is not None:
