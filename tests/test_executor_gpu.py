@@ -119,6 +119,45 @@ def test_whole_layer_runs_equal_controller_batches(cuda, monkeypatch):
         assert docs[0] == docs[1]
 
 
+def test_planning_counts_memoized_per_graph(cuda, monkeypatch):
+    """Full-mode batch counts are a pure function of the graph and the range:
+    a second run on the same DeviceGraph plans the same batches (identical
+    stats document and bytes) without any counting kernel."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels, synth
+    from paper_2211_15082_b200.batching import Thresholds
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import run_inference
+
+    n = 40_000
+    g = synth.gen_products_like(n, n * 25, seed=6, device="cuda")
+    x = synth.gen_features_device(n, 24, seed=6, device="cuda")
+    m = synth.build_gcn(24, 64, 7, 3, seed=1)
+    calls = [0]
+    orig = kernels.IdSet.finalize
+
+    def counting(self, *a, **k):
+        calls[0] += 1
+        return orig(self, *a, **k)
+
+    monkeypatch.setattr(kernels.IdSet, "finalize", counting)
+    runs = []
+    for _ in range(2):
+        before = calls[0]
+        res = run_inference(m, g, x, budget=DeviceBudget(8 << 30),
+                            thresholds=Thresholds(512, 4096), output="device")
+        runs.append((res.output.clone(), res.stats.document(), calls[0] - before))
+    assert runs[0][2] > 0 and runs[1][2] == 0, [r[2] for r in runs]
+    assert torch.equal(runs[0][0], runs[1][0]) and runs[0][1] == runs[1][1]
+    # another graph object with the same content counts again and agrees
+    g2 = synth.gen_products_like(n, n * 25, seed=6, device="cuda")
+    before = calls[0]
+    res = run_inference(m, g2, x, budget=DeviceBudget(8 << 30),
+                        thresholds=Thresholds(512, 4096), output="device")
+    assert calls[0] > before and res.stats.document() == runs[0][1]
+
+
 def test_reassociation_and_precision_agree(golden, cuda):
     """Transform-then-aggregate (narrowing ConvMean) and both GEMM precisions
     agree with the aggregate-first fp32 path within 1e-5 (bar 1e-4)."""
