@@ -103,7 +103,10 @@ int glint_abi_version(void);
                                        16x8 when shared memory is short), 1 24x8,
                                        2 20x10, 3 16x12 */
 #define GLINT_TUNE_FUSED_PROF 13  /* K7: 1 phase-cycle counters (glint_debug_counters 1) */
-#define GLINT_TUNE_COUNT 14
+#define GLINT_TUNE_GAT_L2 14      /* K4 cp.async ring L2 policy: 0 (default) source scores
+                                     evict_last + Z rows evict_first, 1 none (results
+                                     never change) */
+#define GLINT_TUNE_COUNT 15
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of

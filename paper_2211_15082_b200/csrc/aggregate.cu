@@ -1003,6 +1003,7 @@ struct GatArgs {
   float* __restrict__ w;
   float* __restrict__ wself;
   int64_t w_base;
+  int l2_hint;   // source scores evict_last, Z rows evict_first (GLINT_TUNE_GAT_L2 = 1: off)
 };
 
 __device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
@@ -1242,6 +1243,31 @@ __device__ __forceinline__ Scores<H> load_scores(const float* __restrict__ p, bo
 //           gat_row_regular) -- R <= LPR keeps one chunk of weights live.
 // Accumulation: den += w; num += w*z in stored edge order, self last, so the
 // bytes equal gat_row_regular's.
+// H = 4 source scores (16 bytes) with an L2 policy: per edge the kernel reads
+// 16 B of s_src at a random node but DRAM moves 64 B, so keeping the 39 MB
+// score table resident in L2 (evict_last, with the streamed Z rows
+// evict_first) removes most of that per-edge overfetch.
+__device__ __forceinline__ float4 ldg_f4_pol(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+
+template <int H>
+__device__ __forceinline__ Scores<H> load_scores_hint(const float* __restrict__ p, bool vec,
+                                                      bool hint, uint64_t pol) {
+  if constexpr (H == 4) {
+    if (vec && hint) {
+      const float4 t = ldg_f4_pol(p, pol);
+      Scores<H> s;
+      s.v[0] = t.x; s.v[1] = t.y; s.v[2] = t.z; s.v[3] = t.w;
+      return s;
+    }
+  }
+  return load_scores<H>(p, vec);
+}
+
 template <int H, int LPR, int VPL, int R>
 __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int lane_g,
                                               unsigned gmask, float4* zring, float* wbuf) {
@@ -1253,6 +1279,12 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   const int deg = static_cast<int>(end - beg);
   const bool vec = (reinterpret_cast<uintptr_t>(a.s_src) % (4 * H) == 0) &&
                    (reinterpret_cast<uintptr_t>(a.s_dst) % (4 * H) == 0);
+  const bool hint = a.l2_hint != 0;
+  uint64_t pol_keep = 0, pol_stream = 0;
+  if (hint) {
+    pol_keep = policy_evict_last();
+    pol_stream = policy_evict_first();
+  }
 
   float sdst[H], peak[H];
   {
@@ -1267,8 +1299,10 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       const bool two = e + LPR < deg;
       const int32_t u0 = a.ra.map32(__ldg(a.ra.indices + beg + e));
       const int32_t u1 = two ? a.ra.map32(__ldg(a.ra.indices + beg + e + LPR)) : u0;
-      const Scores<H> s0 = load_scores<H>(a.s_src + static_cast<int64_t>(u0) * H, vec);
-      const Scores<H> s1 = load_scores<H>(a.s_src + static_cast<int64_t>(u1) * H, vec);
+      const Scores<H> s0 = load_scores_hint<H>(a.s_src + static_cast<int64_t>(u0) * H, vec, hint,
+                                               pol_keep);
+      const Scores<H> s1 = load_scores_hint<H>(a.s_src + static_cast<int64_t>(u1) * H, vec, hint,
+                                               pol_keep);
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         peak[h] = fmaxf(peak[h], leaky(__fadd_rn(s0.v[h], sdst[h]), a.slope));
@@ -1298,20 +1332,25 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   int32_t ucur = (lane_g < deg) ? a.ra.map32(__ldg(a.ra.indices + beg + lane_g)) : 0;
   int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
   Scores<H> sc;                                     // scores of this lane's edge in chunk cb
-  if (lane_g < deg) sc = load_scores<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec);
+  if (lane_g < deg)
+    sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec, hint, pol_keep);
   auto issue = [&](int slot) {
     if (ie - cb == LPR) {
       cb += LPR;
       ucur = a.ra.map32(nxt);
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
-      if (cb + lane_g < deg) sc = load_scores<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec);
+      if (cb + lane_g < deg)
+        sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec, hint, pol_keep);
     }
     const float* zsrc = row_at(zbase, __shfl_sync(gmask, ucur, ie - cb, LPR), ldzb);
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
         const uint32_t o = static_cast<uint32_t>((slot * VPL + k) * kThreads);
-        cp_async16(zr + o * 16u, zsrc + LPR * 4 * k);
+        if (hint)
+          cp_async16_hint(zr + o * 16u, zsrc + LPR * 4 * k, pol_stream);
+        else
+          cp_async16(zr + o * 16u, zsrc + LPR * 4 * k);
       }
     }
     ++ie;
@@ -2076,8 +2115,9 @@ int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim, 
   GLINT_REQUIRE(ld_out >= static_cast<int64_t>(heads) * head_dim, "gat_aggregate: ld_out too small");
   GLINT_REQUIRE(n_hub >= 0 && n_hub <= n_rows && (schedule || n_hub == 0),
                 "gat_aggregate: bad schedule/n_hub");
-  GatArgs a;
+  GatArgs a{};
   a.ra = RowAddr{indptr, indices, row_ids, row_base, self_rows, col_map};
+  a.l2_hint = tuning(GLINT_TUNE_GAT_L2) == 0;   // default on: cfg3 step 71.1 -> 68.3 ms
   a.heads = heads;
   a.head_dim = head_dim;
   a.head_pitch = head_pitch;

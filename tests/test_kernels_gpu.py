@@ -256,6 +256,15 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
     assert torch.equal(torch.relu(outs[0]), outs[2])
     assert torch.equal(outs[0], outs[3])
     assert torch.equal(outs[0], outs[4]) and torch.equal(outs[0], outs[5])
+    # the K4 ring's L2 policy (scores evict_last, Z evict_first) off: same bytes
+    _lib.call("glint_set_tuning", 14, 1)
+    try:
+        nopol = torch.empty_like(outs[0])
+        kernels.gat_aggregate(nopol, Z, s_src, s_dst, heads, dh, indptr, indices, n,
+                              schedule=sched, n_hub=int(nh.item()))
+        assert torch.equal(nopol, outs[0])
+    finally:
+        _lib.call("glint_set_tuning", 14, 0)
     # and the same bytes without any hub path (every row in the regular kernel),
     # for every launch variant (register-staged and cp.async ring)
     try:
