@@ -49,6 +49,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -240,46 +242,90 @@ class ClockSampler:
 # ------------------------------------------------------------ CPU oracle --
 
 
-def cpu_sample_rate(indptr, indices, x_host, layers, sample_nodes, seed=0):
-    """Time the oracle (the reference algorithm, numpy, 1 thread) on a
-    contiguous block of targets per layer, the way the reference executes one
-    batch (glint/executor.py:351-384).  Returns (nodes/s, seconds, description).
+_CPU_CTX = {}
+
+
+def _cpu_block_layers(bounds):
+    """One worker: targets [lo, hi) through every layer of the sample (the
+    reference's per-batch work, glint/executor.py:351-384).  Returns per-layer
+    seconds."""
+    import contextlib
+
+    from oracle import glint_oracle as orc
+
+    try:
+        from threadpoolctl import threadpool_limits
+        one_blas_thread = threadpool_limits(1)   # one BLAS thread per worker process
+    except Exception:  # noqa: BLE001
+        one_blas_thread = contextlib.nullcontext()
+    c = _CPU_CTX
+    targets = np.arange(bounds[0], bounds[1], dtype=np.int64)
+    per_layer = []
+    with one_blas_thread:
+        for i, spec in enumerate(c["layers"]):
+            h_store = c["x"] if i == 0 else c["stores"][spec["weight"].shape[-1]]
+            t0 = time.perf_counter()
+            bc = orc.build_batch_csc(c["indptr"], c["indices"], targets)   # kernels.py:71-77
+            h = h_store[bc.input_ids]                                        # executor.py:353
+            if spec["kind"] == "ConvMean":
+                out = orc.linear(orc.agg_mean(bc, h), spec["weight"], spec.get("bias"))
+            else:
+                out = orc.agg_attn(bc, h, spec["weight"], spec["attn"])
+            if spec["relu"]:
+                out = orc.elementwise("ReLU", [out])
+            per_layer.append(time.perf_counter() - t0)
+    return per_layer
+
+
+def cpu_sample_rate(indptr, indices, x_host, layers, per_worker, seed=0, workers=1):
+    """Time the oracle (the reference algorithm, numpy) on contiguous blocks of
+    targets, one block per worker process (`workers` host cores, forked, one
+    BLAS thread each), every block through all layers the way the reference
+    executes one batch.  Returns (nodes/s over the wall time, seconds,
+    description).
 
     Layer 1 reads the real features.  Layers 2-3 read a full-size store of
     seeded random rows, because computing the true H^1 for every node is the
     whole CPU run this sample bounds."""
-    import numpy as np
-
-    from oracle import glint_oracle as orc
+    import multiprocessing as mp
 
     n = len(indptr) - 1
     rng = np.random.default_rng(seed)
-    lo = n // 2
-    targets = np.arange(lo, min(n, lo + sample_nodes), dtype=np.int64)
-    per_layer = []
+    lo = n // 2 - (workers * per_worker) // 2
+    lo = max(0, lo)
+    hi = min(n, lo + workers * per_worker)
     stores = {}
     for i, spec in enumerate(layers):
         d_in = spec["weight"].shape[-1]
         if i > 0 and d_in not in stores:      # full-size store of random rows (tiled)
             block = rng.standard_normal((1 << 16, d_in), dtype=np.float32)
             stores[d_in] = np.resize(block, (n, d_in))
-        h_store = x_host if i == 0 else stores[d_in]
+    _CPU_CTX.update(indptr=indptr, indices=indices, x=x_host, layers=layers, stores=stores)
+    cuts = np.linspace(lo, hi, workers + 1).astype(np.int64)
+    blocks = [(int(cuts[k]), int(cuts[k + 1])) for k in range(workers)]
+    if workers == 1:
         t0 = time.perf_counter()
-        bc = orc.build_batch_csc(indptr, indices, targets)          # plan (kernels.py:71-77)
-        h = h_store[bc.input_ids]                                    # store gather (executor.py:353)
-        if spec["kind"] == "ConvMean":
-            out = orc.linear(orc.agg_mean(bc, h), spec["weight"], spec.get("bias"))
-        else:
-            out = orc.agg_attn(bc, h, spec["weight"], spec["attn"])
-        if spec["relu"]:
-            out = orc.elementwise("ReLU", [out])
-        per_layer.append(time.perf_counter() - t0)
-    total = sum(per_layer)
-    rate = len(targets) / total
-    desc = (f"{len(targets)} contiguous targets [{lo}, {lo + len(targets)}) per layer, all "
-            f"{len(layers)} layers (build_batch_csc + gather + aggregate + transform + ReLU); "
-            f"per-layer s {['%.2f' % t for t in per_layer]}")
+        per = [_cpu_block_layers(blocks[0])]
+        total = time.perf_counter() - t0
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:   # forked before the clock starts
+            pool.map(_cpu_block_layers, [(b[0], b[0] + 1) for b in blocks])   # warm the workers
+            t0 = time.perf_counter()
+            per = pool.map(_cpu_block_layers, blocks, chunksize=1)
+            total = time.perf_counter() - t0
+    _CPU_CTX.clear()
+    rate = (hi - lo) / total
+    layer_s = np.max(np.asarray(per), axis=0)
+    desc = (f"{hi - lo} contiguous targets [{lo}, {hi}) in {workers} blocks of ~{per_worker}, "
+            f"one forked worker process per host core, all {len(layers)} layers (build_batch_csc + "
+            f"gather + aggregate + transform + ReLU); slowest worker's per-layer s "
+            f"{['%.2f' % t for t in layer_s]}")
     return rate, total, desc
+
+
+def cpu_workers() -> int:
+    """Host cores the CPU arm uses: all of them (GLINT_CPU_WORKERS overrides)."""
+    return max(1, int(os.environ.get("GLINT_CPU_WORKERS", os.cpu_count() or 1)))
 
 
 def host_inputs(n, und, dim):
@@ -305,8 +351,10 @@ def cpu_block(value, cores, sample, seconds=None):
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
             **({"seconds": seconds} if seconds is not None else {}),
             "cpu_model": workload.cpu_model_name(), "host_cpus": os.cpu_count(),
-            "threads_note": "the reference hot ops (np.add.at, einsum, np.unique) are "
-                            "single-threaded numpy, so one core is what it uses"}
+            "threads_note": "the reference's hot ops (np.add.at, einsum, np.unique) are "
+                            "single-threaded numpy; the arm runs one worker process per "
+                            "host core on disjoint target blocks (the reference's batches "
+                            "are independent), one BLAS thread each"}
 
 
 # ------------------------------------------------------------- reference --
@@ -319,13 +367,14 @@ def run_reference(args, rank, world):
     n, und = sizes(args)
     layers = layer_specs(args.model)
     indptr, indices, x = host_inputs(n, und, 100)
-    sample = args.cpu_sample or 4096
+    sample = args.cpu_sample or 4096          # targets per worker per step
+    workers = cpu_workers()
     for _ in range(max(args.warmup, 0)):
-        cpu_sample_rate(indptr, indices, x, layers, min(sample, 1024))
+        cpu_sample_rate(indptr, indices, x, layers, min(sample, 1024), workers=workers)
     rates, secs = [], []
     sdesc = ""
     for k in range(args.steps):
-        r, s, sdesc = cpu_sample_rate(indptr, indices, x, layers, sample, seed=k)
+        r, s, sdesc = cpu_sample_rate(indptr, indices, x, layers, sample, seed=k, workers=workers)
         rates.append(r)
         secs.append(s)
     value = len(rates) / sum(1.0 / r for r in rates)
@@ -336,7 +385,7 @@ def run_reference(args, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA,
         "impl": "reference",
         "config": config_block(args.model, n, und, world),
-        "cpu_baseline": cpu_block(value, 1, sdesc),
+        "cpu_baseline": cpu_block(value, workers, sdesc),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -725,11 +774,12 @@ def main():
             args, m, g, xt, world, local, agg_of[args.model])
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = args.cpu_sample or 32768      # ~10 s of single-core CPU work
+        sample = args.cpu_sample or 8192       # per worker: ~16 workers x 3 s of CPU work
+        workers = cpu_workers()
         x_host = xt.cpu().numpy()
         rate, secs, sdesc = cpu_sample_rate(host_csr[0], host_csr[1], x_host,
-                                            layer_specs(args.model), sample)
-        line["cpu_baseline"] = cpu_block(rate, 1, sdesc, secs)
+                                            layer_specs(args.model), sample, workers=workers)
+        line["cpu_baseline"] = cpu_block(rate, workers, sdesc, secs)
     if rank == 0:
         print(json.dumps(line), flush=True)
     barrier(world)
