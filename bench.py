@@ -489,7 +489,10 @@ class Runner:
         ms = max_over_ranks(t_start.elapsed_time(t_end) / steps, self.world)
         out = {"value": self.g.num_nodes / (ms / 1e3), "ms_per_step": ms,
                "step_ms": [round(t, 3) for t in step_ms],
-               "gpu_launches": (_lib.LAUNCHES[0] - launches0) // max(steps, 1),
+               # our kernels launched inside the timed region (all steps); the
+               # ncu launch list of the same command is profiles/r02_launches_gcn3.csv
+               "gpu_launches": _lib.LAUNCHES[0] - launches0,
+               "gpu_launches_per_step": (_lib.LAUNCHES[0] - launches0) / max(steps, 1),
                "roofline": roofline(probe.summary(), agg_name, steps, ms),
                "batches_per_step": self.stats.batches,
                "layer_batches": self.stats.layer_batches,

@@ -392,6 +392,8 @@ def spmm_mean(out, h, indptr, indices, n_rows, row_ids=None, row_base=0, self_ro
     _lib.call("glint_spmm_mean_f32", int(n_rows), dim, ptr(indptr), ptr(indices), ptr(row_ids),
               int(row_base), ptr(self_rows), ptr(col_map), ptr(h), ld(h), ptr(out), ld(out),
               ptr(schedule), int(n_hub), ptr(bias), int(act), stream_handle())
+    if int(n_hub) > 0:              # the hub-row kernel beside the regular rows
+        _lib.LAUNCHES[0] += 1
     return out
 
 
@@ -541,6 +543,8 @@ def gat_aggregate(out, Z, s_src, s_dst, heads, head_dim, indptr, indices, n_rows
                   float(LEAKY_SLOPE), ptr(out), ld(out), ptr(schedule), int(n_hub), int(act),
                   base, span, ptr(ws), wsb, stream_handle())
         return out
+    if int(n_hub) > 0:              # the hub-row kernel beside the regular rows
+        _lib.LAUNCHES[0] += 1
     _lib.call("glint_gat_aggregate_f32", int(n_rows), heads, head_dim, head_pitch(head_dim),
               ptr(indptr), ptr(indices), ptr(row_ids), int(row_base), ptr(self_rows),
               ptr(col_map), ptr(Z), ld(Z), ptr(s_src), ptr(s_dst), float(LEAKY_SLOPE), ptr(out),
