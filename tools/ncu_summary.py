@@ -107,8 +107,8 @@ def main():
     for rep in args[1:]:
         recs += raw(rep)
     out = {"kernels": recs}
-    md = ["| kernel | ms | DRAM read GB | DRAM write GB | DRAM % peak | tensor pipe % | warps active % | regs |",
-          "|---|---|---|---|---|---|---|---|"]
+    md = (["| kernel | ms | DRAM read GB | DRAM write GB | DRAM % peak | tensor pipe % | warps active % | regs |",
+           "|---|---|---|---|---|---|---|---|"] if recs else [])
     for r in recs:
         md.append("| {} | {:.3f} | {:.2f} | {:.2f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} |".format(
             short(r["kernel"]), r.get("duration_ms", 0), r.get("dram_read_bytes", 0) / 1e9,
