@@ -157,6 +157,23 @@ int glint_degree_schedule(int64_t n_rows, const int64_t* indptr,
                           int64_t* n_hub_out, void* workspace,
                           size_t workspace_bytes, glint_stream_t stream);
 
+/* ----------------------------------------------- RCMK on the device
+ * Building blocks of reorder.rcmk for a DeviceGraph (reference reorder.py:
+ * 72-123), over the symmetrised adjacency (ptr int64 [n+1], adj int32, every
+ * row distinct neighbours without self loops, ordered by (degree, id)).
+ * components: comp_out[v] = the minimum id of v's connected component.
+ * starts: start_key[c] = min over members v of component c of
+ *   (degree(v) << 32 | v); untouched entries are UINT64_MAX.
+ * expand: for i < n_front and every neighbour u of frontier[i] with
+ *   level[u] < 0: best[u] = min(best[u], i). */
+int glint_rcmk_components(int64_t n, const int64_t* ptr, const int32_t* adj,
+                          int32_t* comp_out, glint_stream_t stream);
+int glint_rcmk_starts(int64_t n, const int64_t* ptr, const int32_t* comp,
+                      uint64_t* start_key, glint_stream_t stream);
+int glint_rcmk_expand(int64_t n_front, const int32_t* frontier, const int64_t* ptr,
+                      const int32_t* adj, const int32_t* level, int64_t* best,
+                      glint_stream_t stream);
+
 /* ------------------------------------------------------ K2 dense transform
  * Replaces kernels.py:95-107 linear (einsum "ij,kj->ik" + bias), with an
  * optional fused activation (elementwise ReLU/LeakyReLU, kernels.py:206-215).

@@ -82,6 +82,9 @@ SIGNATURES = {
     "glint_relabel_csc": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P]),
     "glint_narrow_ids": (ctypes.c_int, [_I64, _P, _P, _I64, _P, _P]),
     "glint_rcmk_host": (ctypes.c_int, [_I64, _P, _P, _P]),
+    "glint_rcmk_components": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
+    "glint_rcmk_starts": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
+    "glint_rcmk_expand": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P]),
     "glint_rcmk_sorted_host": (ctypes.c_int, [_I64, _P, _P, _P]),
     "glint_narrow_ids_host": (_I64, [_P, _P, _I64, _I32]),
     "glint_upload_start": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _P, _P]),
@@ -126,7 +129,7 @@ def last_error() -> str:
 
 # Kernels launched per call (for the bench's launch count); host-only or
 # memset-only entry points launch none.
-KERNELS_PER_CALL = {"glint_conv_mean_f32": 2, "glint_degree_schedule": 3, "glint_idset_finalize": 4,
+KERNELS_PER_CALL = {"glint_conv_mean_f32": 2, "glint_rcmk_components": 3, "glint_degree_schedule": 3, "glint_idset_finalize": 4,
                     "glint_degree_prefix": 3, "glint_hub_prefix": 3, "glint_idset_clear": 0, "glint_rcmk_host": 0,
                     "glint_rcmk_sorted_host": 0, "glint_sample_neighbors": 4,
                     "glint_gat_aggregate_ws_f32": 2, "glint_upload_start": 0, "glint_upload_start_packed": 1, "glint_copy_rows_async": 0,

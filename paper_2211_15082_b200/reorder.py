@@ -87,7 +87,8 @@ def _sorted_adjacency_device(dg):
     of self loops and ordered by (degree, id) -- the order the RCMK BFS visits
     candidates in (reorder.py:89-99).  Two device sorts: (row, col) to merge
     duplicates and count degrees, then (row, rank of col by (degree, id)).
-    Returns host (ptr int64 [n+1], adj int32 [nnz])."""
+    Returns device (ptr int64 [n+1], adj int32 [nnz], rank int64 [n]: each
+    node's position in the (degree, id) order)."""
     import torch
 
     n = int(dg.num_nodes)
@@ -111,20 +112,86 @@ def _sorted_adjacency_device(dg):
     adj = order[key2 % n].to(torch.int32)
     ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(deg, 0, out=ptr[1:])
-    return ptr.cpu().numpy(), adj.cpu().numpy()
+    return ptr, adj, rank
+
+
+# Level cap of the device BFS: path-like graphs with thousands of BFS levels
+# are faster on the host's linear queue than one device round trip per level.
+RCMK_MAX_DEVICE_LEVELS = 4096
+
+
+def _rcmk_device(dg):
+    """RCMK on the device, the same permutation as the sequential reference
+    (reorder.py:72-123): components by union-find, starts = each component's
+    minimum (degree, id) member, components in ascending start order, then a
+    level-synchronous BFS over every component at once in which a node's
+    parent is its first neighbour in the previous level's sequence and each
+    level is ordered by (parent index, (degree, id) rank) -- exactly the order
+    the sequential queue appends nodes in.  Returns perm (host int64), or None
+    past RCMK_MAX_DEVICE_LEVELS levels."""
+    import torch
+
+    from . import kernels
+
+    n = int(dg.num_nodes)
+    dev = dg.indptr.device
+    ptr, adj, rank = _sorted_adjacency_device(dg)
+    st = kernels.stream_handle()
+    comp = torch.empty(n, dtype=torch.int32, device=dev)
+    _lib.call("glint_rcmk_components", n, kernels.ptr(ptr), kernels.ptr(adj), kernels.ptr(comp), st)
+    start_key = torch.empty(n, dtype=torch.int64, device=dev)
+    _lib.call("glint_rcmk_starts", n, kernels.ptr(ptr), kernels.ptr(comp), kernels.ptr(start_key), st)
+    ids = torch.arange(n, device=dev, dtype=torch.int64)
+    roots = torch.nonzero(comp.to(torch.int64) == ids).flatten()
+    starts = torch.sort(start_key[roots] & 0xFFFFFFFF).values          # component order
+    comp_rank = torch.empty(n, dtype=torch.int64, device=dev)
+    comp_rank[comp[starts].to(torch.int64)] = torch.arange(len(starts), device=dev)
+    level = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    gidx = torch.empty(n, dtype=torch.int64, device=dev)
+    best = torch.full((n,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    none = torch.iinfo(torch.int64).max
+    frontier = starts.to(torch.int32)
+    level[starts] = 0
+    gidx[starts] = torch.arange(len(starts), device=dev)
+    depth = 0
+    while len(frontier):
+        if depth >= RCMK_MAX_DEVICE_LEVELS:
+            return None
+        _lib.call("glint_rcmk_expand", len(frontier), kernels.ptr(frontier), kernels.ptr(ptr),
+                  kernels.ptr(adj), kernels.ptr(level), kernels.ptr(best), st)
+        cand = torch.nonzero(best != none).flatten()
+        if len(cand) == 0:
+            break
+        order = torch.sort(best[cand] * n + rank[cand]).indices
+        nxt = cand[order]
+        best[cand] = none
+        depth += 1
+        level[nxt] = depth
+        gidx[nxt] = torch.arange(len(nxt), device=dev)
+        frontier = nxt.to(torch.int32)
+    # sequence = (component, level, index in level); RCMK reverses it
+    seq = torch.sort(gidx, stable=True).indices
+    key1 = comp_rank[comp[seq].to(torch.int64)] * (depth + 1) + level[seq].to(torch.int64)
+    seq = seq[torch.sort(key1, stable=True).indices]
+    return seq.flip(0).cpu().numpy().astype(np.int64)
 
 
 def rcmk(g) -> NodeOrder:
     """Reverse Cuthill-McKee over in- plus out-edges.
 
-    A DeviceGraph gets its (degree, id)-sorted symmetric adjacency built on the
-    device and a linear native BFS; a host CscGraph runs the all-host native
-    version (same tie rules, same permutation).
+    A DeviceGraph runs entirely on the device (_rcmk_device: union-find
+    components and a level-synchronous BFS; a linear native BFS on the host for
+    graphs deeper than RCMK_MAX_DEVICE_LEVELS); a host CscGraph runs the
+    all-host native version (same tie rules, same permutation).
     """
     from .storage import DeviceGraph
 
     if isinstance(g, DeviceGraph) and int(g.num_nodes) > 0:
-        ptr, adj = _sorted_adjacency_device(g)
+        perm = _rcmk_device(g)
+        if perm is not None:
+            return NodeOrder(perm)
+        ptr, adj, _ = _sorted_adjacency_device(g)      # deep BFS: the host's queue
+        ptr, adj = ptr.cpu().numpy(), adj.cpu().numpy()
         n = int(g.num_nodes)
         perm = np.empty(n, dtype=np.int64)
         rc = _lib.load().glint_rcmk_sorted_host(n, ptr.ctypes.data_as(ctypes.c_void_p),

@@ -481,6 +481,36 @@ def test_device_rcmk_matches_reference_and_host_path(golden, cuda):
         assert np.array_equal(host, dev), (n, e)
 
 
+def test_device_rcmk_bfs_levels_and_fallback(cuda, monkeypatch):
+    """The level-synchronous device BFS (union-find components, first-parent
+    ordering) equals the sequential native RCMK on a heavy-tailed graph with
+    isolated nodes and many components, on a path (one node per level), and
+    through the host fallback once the level cap is hit."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels, reorder, synth
+    from paper_2211_15082_b200.storage import CscGraph
+
+    dg = synth.gen_products_like(60_000, 60_000 * 12, seed=9, device="cuda")
+    hg = CscGraph(dg.num_nodes, dg.num_edges, dg.indptr_host,
+                  dg.indices.to(torch.int64).cpu().numpy())
+    want = reorder.rcmk(hg).perm
+    assert np.array_equal(reorder.rcmk(dg).perm, want)
+    # a path 0-1-...-999 plus isolated nodes and a triangle: 1000 BFS levels
+    n = 1010
+    edges = [(i + 1, i) for i in range(999)] + [(1001, 1000), (1002, 1001), (1000, 1002)]
+    dst = np.array([d for d, _ in edges])
+    srcs = np.array([s_ for _, s_ in edges])
+    order = np.argsort(dst, kind="stable")
+    indptr = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+    g = CscGraph(n, len(edges), indptr, srcs[order].astype(np.int64))
+    want = reorder.rcmk(g).perm
+    assert np.array_equal(reorder.rcmk(kernels.device_graph(g)).perm, want)
+    monkeypatch.setattr(reorder, "RCMK_MAX_DEVICE_LEVELS", 10)
+    assert reorder._rcmk_device(kernels.device_graph(g)) is None
+    assert np.array_equal(reorder.rcmk(kernels.device_graph(g)).perm, want)
+
+
 def test_device_sampling_matches_reference(golden, cuda):
     """glint_sample_neighbors == the reference's draws (golden) and == the host
     restatement on random graphs with duplicates, for all-node and subset draws."""
