@@ -1517,7 +1517,10 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
 
     if probe is not None:
         probe.mark("run_inference entry")
-    node_order = make_order(g, order, seed)
+    # RCMK of a host graph runs on its device copy (reorder._rcmk_device),
+    # once the CSR has landed; the other orders are cheap host numpy
+    rcmk_on_device = order == "rcmk" and isinstance(g, CscGraph) and g.num_nodes > 0
+    node_order = None if rcmk_on_device else make_order(g, order, seed)
     if isinstance(g, CscGraph) and _host_tensor_ok(x_store):
         # Host inputs: features first, then the CSR in row chunks on a copy
         # stream; layer-1 batches start as soon as their rows have arrived.
@@ -1550,11 +1553,13 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             probe.mark("csr uploaded (copy stream)", copy)
             probe.mark("uploads issued (main stream)")
         torch.cuda.current_stream(dev).wait_event(x_ready)
-        if not node_order.is_identity():
+        if node_order is None or not node_order.is_identity():
             dg0.wait_rows()
     else:
         dg0 = kernels.device_graph(g)
         x0 = _as_device_store(x_store, dg0.device)
+    if node_order is None:
+        node_order = make_order(dg0, order, seed)
     g_i, x_i = apply_order_device(dg0, x0, node_order)
     if mode == "full" or targets is None:
         internal = user_targets                      # sorted(inv[arange(N)]) == arange(N)
