@@ -658,6 +658,7 @@ extern "C" int glint_conv_mean_f32(int64_t n_rows, int32_t dim_in, int32_t dim_o
   GLINT_REQUIRE(max_ctas >= 0, "conv_mean: max_ctas must be >= 0");
   GLINT_REQUIRE(workspace_bytes >= glint_conv_mean_workspace_bytes(dim_in, dim_out),
                 "conv_mean: workspace too small");
+  GLINT_REQUIRE(aligned16(workspace), "conv_mean: workspace must be 16-byte aligned");
   if (!glint_conv_mean_supported(dim_in, dim_out) || ld_h % 4 != 0 || ld_out % 4 != 0 ||
       !aligned16(h) || !aligned16(out) || n_rows > (1LL << 31) * fused::ROWS)
     return GLINT_EUNSUPPORTED;

@@ -44,6 +44,33 @@ def test_argument_errors_map_to_value_error_without_gpu():
     assert "heads" in _lib.last_error()
 
 
+def test_conv_mean_argument_errors_without_gpu():
+    """K7's host-side validation (glint_conv_mean_f32) runs before any CUDA call."""
+    args = dict(n_rows=10, dim_in=100, dim_out=256)
+
+    def call(**kw):
+        a = {**args, **kw}
+        ws = 0 if kw.get("no_ws") else 4096
+        _lib.call("glint_conv_mean_f32", a["n_rows"], a["dim_in"], a["dim_out"], 8, 16, None, 0,
+                  None, None, 32, 100, 48, 100, None, kw.get("act", 0), 64, 256, None,
+                  kw.get("max_ctas", 0), None if kw.get("no_ws") else 80, ws, None)
+
+    with pytest.raises(ValueError, match="n_rows"):
+        call(n_rows=-1)
+    with pytest.raises(ValueError, match="act"):
+        call(act=7)
+    with pytest.raises(ValueError, match="max_ctas"):
+        call(max_ctas=-2)
+    with pytest.raises(ValueError, match="null"):
+        call(no_ws=True)
+    with pytest.raises(ValueError, match="workspace too small"):
+        call()
+    assert _lib.query("glint_conv_mean_supported", 100, 256) == 1
+    assert _lib.query("glint_conv_mean_supported", 256, 256) == 0
+    assert _lib.query("glint_conv_mean_supported", 100, 300) == 0
+    assert _lib.query("glint_conv_mean_workspace_bytes", 100, 256) >= 256 + 13 * 2 * 256 * 8 * 4
+
+
 def test_workspace_queries():
     assert _lib.query("glint_idset_workspace_bytes", 1000) >= 1000 // 8
     assert _lib.query("glint_scan_workspace_bytes", 10) >= 16
