@@ -777,7 +777,7 @@ def main():
             args, m, g, xt, world, local, agg_of[args.model])
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = args.cpu_sample or 8192       # per worker: ~16 workers x 3 s of CPU work
+        sample = args.cpu_sample or 4096       # per worker: ~16 workers x 1.5 s of CPU work
         workers = cpu_workers()
         x_host = xt.cpu().numpy()
         rate, secs, sdesc = cpu_sample_rate(host_csr[0], host_csr[1], x_host,
