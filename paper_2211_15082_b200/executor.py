@@ -28,7 +28,6 @@ are computed on the host as in the reference and uploaded.
 from __future__ import annotations
 
 import os
-import sys
 import time
 from dataclasses import dataclass, field
 
@@ -895,9 +894,6 @@ class LayerwiseEngine:
                 if self.probe is not None:
                     self.probe.begin("conv_mean")
                 split = not self._fused_ok
-                if os.environ.get("GLINT_DEBUG_FUSED"):
-                    print(f"conv_mean L{blk.layer} [{s},{e}) max_ctas={self._fused_ctas} "
-                          f"split_hubs={n_hub if split else 0}", file=sys.stderr, flush=True)
                 if split:
                     self._hub_rows_beside_k7(out, h, cmap, o, act, gl, row_ids, row_base, sched,
                                              n_hub, B)
