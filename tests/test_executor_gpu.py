@@ -278,6 +278,28 @@ def test_two_ranks_on_one_gpu_bit_identical(tmp_path):
 
 
 @pytest.mark.gpu
+def test_exchange_nccl_calls_on_one_gpu():
+    """The NCCL calls of the row exchange (grouped broadcasts through the
+    coalescing manager, the halo all-to-all, direct tensor exchanges) run in a
+    1-rank NCCL group inside the engine; outputs bit-identical to no exchange."""
+    import json
+    import os
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29571")
+    out = subprocess.run([sys.executable, str(root / "tools" / "nccl_single_check.py"), "20000"],
+                         env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    runs = [x for x in lines if "model" in x]
+    assert len(runs) == 4 and all(x["bit_identical"] and x["backend"] == "nccl" for x in runs)
+    assert any("direct_exchanges" in x for x in lines)
+
+
+@pytest.mark.gpu
 def test_bench_json_contract():
     """bench.py (small graph) prints one JSON line carrying every key the driver
     reads, for both arms."""
