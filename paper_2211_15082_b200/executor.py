@@ -914,8 +914,8 @@ class LayerwiseEngine:
                 agg = torch.empty((B, pitch_of(d_in)), dtype=torch.float32, device=self.dev)[:, :d_in]
                 if self.probe is not None:
                     self.probe.begin("spmm_mean")
-                kernels.spmm_mean(agg, h, gl.indptr, gl.indices, B, row_ids=row_ids,
-                                  row_base=row_base, col_map=cmap, schedule=sched, n_hub=n_hub)
+                kernels.spmm_mean_hot(agg, h, gl, B, row_ids=row_ids, row_base=row_base,
+                                      col_map=cmap, schedule=sched, n_hub=n_hub)
                 if self.probe is not None:
                     self.probe.end(agg_bytes(d_in, plan.num_edges, B))
                 act_op = fused.get(o)

@@ -397,6 +397,47 @@ def spmm_mean(out, h, indptr, indices, n_rows, row_ids=None, row_base=0, self_ro
     return out
 
 
+# L2 steering of K1's widest gathers: the source ids of the most-read rows
+# (highest out-degree, as many as fit GLINT_K1_HOT_MB of L2) carry bit 31 in a
+# per-graph annotated copy of `indices`, and K1 loads them evict_last and the
+# rest evict_first (GLINT_TUNE_L2_HINT = 1).  Only rows of >= HOT_MIN_ROW_BYTES:
+# profiles/r02_l2_hint_probe.jsonl measured up to 3.6% at d=256 and nothing at
+# d=48 / d=100.  0 disables.
+HOT_MB = int(os.environ.get("GLINT_K1_HOT_MB", "80"))
+HOT_MIN_ROW_BYTES = 1024
+
+
+def hot_indices(dg, row_bytes):
+    """The DeviceGraph's indices with bit 31 set on ids of its hottest source
+    rows (cached per graph and row size), or None when steering is off."""
+    torch = _torch()
+    if HOT_MB <= 0 or row_bytes < HOT_MIN_ROW_BYTES or dg.num_edges == 0:
+        return None
+    rows = min(int(dg.num_nodes), (HOT_MB << 20) // int(row_bytes))
+    key = ("hot_indices", rows)
+    hit = dg._cache.get(key)
+    if hit is None:
+        idx = dg.indices
+        cnt = torch.bincount(idx.long(), minlength=int(dg.num_nodes))
+        hot = torch.zeros(int(dg.num_nodes), dtype=torch.bool, device=idx.device)
+        hot[torch.topk(cnt, rows).indices] = True
+        flag = torch.tensor(-2 ** 31, dtype=torch.int32, device=idx.device)
+        hit = dg._cache[key] = torch.where(hot[idx.long()], idx | flag, idx)
+    return hit
+
+
+def spmm_mean_hot(out, h, dg, n_rows, **kw):
+    """K1 with the hot-row L2 policy when it applies (same bytes as spmm_mean)."""
+    ann = hot_indices(dg, ld(h) * 4) if kw.get("col_map") is None else None
+    if ann is None:
+        return spmm_mean(out, h, dg.indptr, dg.indices, n_rows, **kw)
+    _lib.call("glint_set_tuning", 11, 1)
+    try:
+        return spmm_mean(out, h, dg.indptr, ann, n_rows, **kw)
+    finally:
+        _lib.call("glint_set_tuning", 11, 0)
+
+
 _SMS = {}
 
 

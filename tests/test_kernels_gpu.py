@@ -667,3 +667,27 @@ def test_async_upload_wide_ids_use_int32(cuda):
     dg.wait_rows()
     torch.cuda.synchronize()
     assert dg.indices.cpu().numpy().tolist() == ids.tolist()
+
+
+def test_k1_hot_row_l2_steering_same_bytes(cuda, monkeypatch):
+    """K1 on the hot-annotated index copy (bit 31 on the most-read source ids,
+    evict_last for them and evict_first for the rest) gives the same bytes;
+    the annotated ids mask back to the graph's ids."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels, synth
+
+    g = synth.gen_products_like(30_000, 30_000 * 20, seed=3, device="cuda")
+    monkeypatch.setattr(kernels, "HOT_MB", 4)           # a few thousand hot rows
+    h = torch.randn((g.num_nodes, 256), device="cuda")
+    sched, nh = kernels.degree_schedule(g.indptr, None, 0, g.num_nodes)
+    ann = kernels.hot_indices(g, 256 * 4)
+    assert ann is not None and int((ann < 0).sum()) > 0
+    assert torch.equal(ann & 0x7FFFFFFF, g.indices)
+    want = torch.empty_like(h)
+    kernels.spmm_mean(want, h, g.indptr, g.indices, g.num_nodes, schedule=sched,
+                      n_hub=int(nh.item()))
+    got = torch.empty_like(h)
+    kernels.spmm_mean_hot(got, h, g, g.num_nodes, schedule=sched, n_hub=int(nh.item()))
+    assert torch.equal(got, want)
+    assert kernels.hot_indices(g, 48 * 4) is None        # narrow rows: no steering
