@@ -1329,26 +1329,35 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   const char* zbase = reinterpret_cast<const char*>(a.Z + lane_g * 4);
   const int32_t ldzb = static_cast<int32_t>(a.ldz * 4);
   int ie = 0, cb = 0;
-  int32_t ucur = (lane_g < deg) ? a.ra.map32(__ldg(a.ra.indices + beg + lane_g)) : 0;
+  // ucur: the mapped source row of this lane's edge in chunk cb, with the
+  // stored id's bit 31 ("hot" row, kernels.hot_indices) carried along
+  auto mapped = [&](int32_t raw) {
+    return a.ra.map32(raw) | static_cast<int32_t>(static_cast<uint32_t>(raw) & 0x80000000u);
+  };
+  int32_t ucur = (lane_g < deg) ? mapped(__ldg(a.ra.indices + beg + lane_g)) : 0;
   int32_t nxt = (LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + LPR + lane_g) : 0;
   Scores<H> sc;                                     // scores of this lane's edge in chunk cb
   if (lane_g < deg)
-    sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec, hint, pol_keep);
+    sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur & 0x7fffffff) * H, vec, hint,
+                             pol_keep);
   auto issue = [&](int slot) {
     if (ie - cb == LPR) {
       cb += LPR;
-      ucur = a.ra.map32(nxt);
+      ucur = mapped(nxt);
       nxt = (cb + LPR + lane_g < deg) ? __ldg(a.ra.indices + beg + cb + LPR + lane_g) : 0;
       if (cb + lane_g < deg)
-        sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur) * H, vec, hint, pol_keep);
+        sc = load_scores_hint<H>(a.s_src + static_cast<int64_t>(ucur & 0x7fffffff) * H, vec,
+                                 hint, pol_keep);
     }
-    const float* zsrc = row_at(zbase, __shfl_sync(gmask, ucur, ie - cb, LPR), ldzb);
+    const int32_t uh = __shfl_sync(gmask, ucur, ie - cb, LPR);
+    const float* zsrc = row_at(zbase, uh & 0x7fffffff, ldzb);
+    const uint64_t pol = uh < 0 ? pol_keep : pol_stream;   // hot Z rows stay in L2
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       if (ok[k]) {
         const uint32_t o = static_cast<uint32_t>((slot * VPL + k) * kThreads);
         if (hint)
-          cp_async16_hint(zr + o * 16u, zsrc + LPR * 4 * k, pol_stream);
+          cp_async16_hint(zr + o * 16u, zsrc + LPR * 4 * k, pol);
         else
           cp_async16(zr + o * 16u, zsrc + LPR * 4 * k);
       }

@@ -945,7 +945,10 @@ class LayerwiseEngine:
                        "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
                 if self.probe is not None:
                     self.probe.begin("gat_aggregate")
-                kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, gl.indptr, gl.indices, B,
+                hot = (kernels.hot_indices(gl, kernels.ld(Z) * 4, reserve=GAT_SCORE_L2)
+                       if cmap is None else None)
+                kernels.gat_aggregate(out, Z, s_src, s_dst, H, dh, gl.indptr,
+                                      gl.indices if hot is None else hot, B,
                                       row_ids=row_ids, row_base=row_base, col_map=cmap,
                                       schedule=sched, n_hub=n_hub, act=act)
                 if self.probe is not None:
@@ -1119,6 +1122,11 @@ def agg_bytes(width, n_edges, n_rows, heads=0) -> int:
     if heads:
         b += 4 * heads * (n_edges + 2 * n_rows)
     return b
+
+
+# L2 already held for K4's evict_last source-score table (N x heads fp32) when
+# hot Z rows are steered beside it (Products: 39 MB)
+GAT_SCORE_L2 = 40 << 20
 
 
 def conv_bytes(d_in, d_out, n_edges, n_rows) -> int:

@@ -407,13 +407,16 @@ HOT_MB = int(os.environ.get("GLINT_K1_HOT_MB", "80"))
 HOT_MIN_ROW_BYTES = 1024
 
 
-def hot_indices(dg, row_bytes):
+def hot_indices(dg, row_bytes, reserve=0):
     """The DeviceGraph's indices with bit 31 set on ids of its hottest source
-    rows (cached per graph and row size), or None when steering is off."""
+    rows (cached per graph and row count), or None when steering is off.
+    `reserve` bytes of the HOT_MB budget are already held by other evict_last
+    data (K4's score table)."""
     torch = _torch()
-    if HOT_MB <= 0 or row_bytes < HOT_MIN_ROW_BYTES or dg.num_edges == 0:
+    budget = (HOT_MB << 20) - int(reserve)
+    if HOT_MB <= 0 or budget <= 0 or row_bytes < HOT_MIN_ROW_BYTES or dg.num_edges == 0:
         return None
-    rows = min(int(dg.num_nodes), (HOT_MB << 20) // int(row_bytes))
+    rows = min(int(dg.num_nodes), budget // int(row_bytes))
     key = ("hot_indices", rows)
     hit = dg._cache.get(key)
     if hit is None:
