@@ -742,6 +742,7 @@ def main():
                    "reassociate": True},
         "batches_per_step": meas["batches_per_step"], "layer_batches": meas["layer_batches"],
         "roofline": meas["roofline"], "gpu_launches": meas["gpu_launches"],
+        "gpu_launches_per_step": meas["gpu_launches_per_step"],
         "clocks": meas["clocks"], "step_ms": meas["step_ms"],
         **({"tuning": args.tune} if args.tune else {}),
     }

@@ -420,6 +420,13 @@ def hot_indices(dg, row_bytes, reserve=0):
     key = ("hot_indices", rows)
     hit = dg._cache.get(key)
     if hit is None:
+        # built on the graph's second request: the annotation pass (~1 ms on
+        # the Products graph) outweighs its gain for a graph used once (an e2e
+        # call uploads a fresh DeviceGraph each time)
+        seen = dg._cache.get(("hot_requests", rows), 0)
+        dg._cache[("hot_requests", rows)] = seen + 1
+        if seen < 1:
+            return None
         idx = dg.indices
         cnt = torch.bincount(idx.long(), minlength=int(dg.num_nodes))
         hot = torch.zeros(int(dg.num_nodes), dtype=torch.bool, device=idx.device)

@@ -681,6 +681,7 @@ def test_k1_hot_row_l2_steering_same_bytes(cuda, monkeypatch):
     monkeypatch.setattr(kernels, "HOT_MB", 4)           # a few thousand hot rows
     h = torch.randn((g.num_nodes, 256), device="cuda")
     sched, nh = kernels.degree_schedule(g.indptr, None, 0, g.num_nodes)
+    assert kernels.hot_indices(g, 256 * 4) is None        # first request: not built yet
     ann = kernels.hot_indices(g, 256 * 4)
     assert ann is not None and int((ann < 0).sum()) > 0
     assert torch.equal(ann & 0x7FFFFFFF, g.indices)
