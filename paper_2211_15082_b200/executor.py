@@ -141,6 +141,16 @@ def _expand_dev(dg, nodes_np):
     return ids.extract().cpu().numpy()
 
 
+def _sorted_unique(a):
+    """np.unique(a) without the hash/sort when `a` is already strictly
+    increasing (the usual target list): an O(n) check instead of ~30 ms for
+    245K ids on the box's CPU."""
+    a = np.asarray(a, dtype=np.int64)
+    if len(a) < 2 or bool(np.all(a[1:] > a[:-1])):
+        return a
+    return np.unique(a)
+
+
 def skip_fires(n_next, graph) -> bool:
     """|V[l+1]| * d_avg >= n, exact in integers (glint/executor.py:124-126)."""
     return n_next * graph.num_edges >= graph.num_nodes * graph.num_nodes
@@ -153,7 +163,7 @@ def annotate(g, targets, depth, mode, fanout=None, seed=0) -> TargetSets:
     n = g.num_nodes
     targets = np.asarray(targets, dtype=np.int64)
     if not (mode == "full" and len(targets) == n and _is_arange(targets)):
-        targets = np.unique(targets)
+        targets = _sorted_unique(targets)
     if len(targets) and (targets[0] < 0 or targets[-1] >= n):
         raise ConfigError("target ids out of range")
     sampled = None
@@ -1512,7 +1522,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         user_targets = arange_ids(g.num_nodes)
     else:
         user_targets = np.asarray(targets, dtype=np.int64)
-        if len(user_targets) != len(np.unique(user_targets)):
+        if len(user_targets) != len(_sorted_unique(user_targets)):
             raise ConfigError("duplicate target ids")
         if len(user_targets) and (user_targets.min() < 0 or user_targets.max() >= g.num_nodes):
             raise ConfigError("target ids out of range")
