@@ -434,7 +434,7 @@ class Runner:
         self.x = _as_device_store(x, g.indptr.device)
         self.schedule = split(m)
         self.tsets = annotate(g, np.arange(0), m.depth, "full")
-        resident = _resident_bytes(m, self.schedule, self.tsets, g)
+        resident = _resident_bytes(m, self.schedule, self.tsets, g, reassociate=True)
         budget = DeviceBudget.from_device(reserve_bytes=resident + (2 << 30))
         self.budget = DeviceBudget(int(min_over_ranks(budget.capacity, world)))
         self.th0 = Thresholds(1024, 32768)

@@ -1588,7 +1588,7 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     schedule = None
     if executor == "layerwise":
         schedule = split(m)
-        bud = resolve_budget(budget, _resident_bytes(m, schedule, tsets, g_i))
+        bud = resolve_budget(budget, _resident_bytes(m, schedule, tsets, g_i, reassociate))
         ex = _exchange_for(distributed, mode, g_i, exchange)
         eng = LayerwiseEngine(m, schedule, g_i, x_i, tsets, bud, thresholds, stats, precision,
                               row_range=ex.row_range if ex else None, reassociate=reassociate)
@@ -1638,8 +1638,26 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
                            order=node_order, schedule=schedule, budget=bud)
 
 
-def _resident_bytes(m, schedule, tsets, g):
-    """Upper bound of resident store bytes alive at once (for budget='device')."""
+def _transform_bytes(m, blk, src_rows, reassociate):
+    """Bytes of a block's per-layer transformed source rows (transform-first
+    convs: ConvAttn's Z and scores, a reassociated narrowing ConvMean's z),
+    alive while the block runs, outside the per-batch footprint model."""
+    total = 0
+    for o in blk.op_ids:
+        op = m.operators[o]
+        if op.kind == "ConvAttn":
+            H, dh = int(op.params["weight"].shape[0]), int(op.params["weight"].shape[1])
+            total += src_rows * (H * kernels.head_pitch(dh) + 2 * H) * 4
+        elif op.kind == "ConvMean" and reassociate:
+            w = op.params["weight"]
+            if pitch_of(w.shape[0]) < pitch_of(w.shape[1]):
+                total += src_rows * pitch_of(w.shape[0]) * 4
+    return total
+
+
+def _resident_bytes(m, schedule, tsets, g, reassociate=False):
+    """Upper bound of resident bytes alive at once (for budget='device'): the
+    stores, plus the running block's transformed source rows."""
     live = 0
     peak = 0
     sizes = {}
@@ -1648,7 +1666,9 @@ def _resident_bytes(m, schedule, tsets, g):
         for o in blk.outputs:
             sizes[TensorRef(blk.block_id, o).key] = rows * pitch_of(m.out_dims[o]) * 4
             live += sizes[TensorRef(blk.block_id, o).key]
-        peak = max(peak, live)
+        src_rows = len(tsets.v_sets[blk.layer - 1]) if blk.layer > 1 and \
+            (blk.layer - 1) in tsets.v_sets else g.num_nodes
+        peak = max(peak, live + _transform_bytes(m, blk, src_rows, reassociate))
         for key, last in schedule.drop_after.items():
             if last == blk.block_id and key in sizes:
                 live -= sizes.pop(key)

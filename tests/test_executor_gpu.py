@@ -158,6 +158,40 @@ def test_planning_counts_memoized_per_graph(cuda, monkeypatch):
     assert calls[0] > before and res.stats.document() == runs[0][1]
 
 
+def test_real_allocations_stay_within_the_budget(cuda):
+    """The batch controller's capacity bounds the real per-batch allocations:
+    peak device memory during a run, minus the resident bytes the budget does
+    not cover (stores and a transform-first conv's transformed rows,
+    executor._resident_bytes), stays under the capacity (the reference's
+    footprint model is an upper bound of what the engine allocates per batch)."""
+    import torch
+
+    from paper_2211_15082_b200 import synth
+    from paper_2211_15082_b200.batching import Thresholds
+    from paper_2211_15082_b200.device import DeviceBudget
+    from paper_2211_15082_b200.executor import _resident_bytes, annotate, run_inference
+    from paper_2211_15082_b200.splitter import split
+
+    n = 40_000
+    g = synth.gen_products_like(n, n * 25, seed=7, device="cuda")
+    x = synth.gen_features_device(n, 24, seed=7, device="cuda")
+    for m in (synth.build_gcn(24, 64, 7, 3, seed=1), synth.build_gat(24, 16, 7, 2, heads=4, seed=2)):
+        cap = 6 << 20
+        resident = _resident_bytes(m, split(m), annotate(g, np.arange(0), m.depth, "full"), g)
+        run_inference(m, g, x, budget=DeviceBudget(cap), thresholds=Thresholds(512, 4096),
+                      output="device")                       # warm caches (schedules, id sets)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        res = run_inference(m, g, x, budget=DeviceBudget(cap), thresholds=Thresholds(512, 4096),
+                            output="device")
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base
+        assert res.stats.batches > m.depth                    # really batched
+        assert peak - resident <= cap, (m.depth, peak, resident, cap)
+
+
 def test_reassociation_and_precision_agree(golden, cuda):
     """Transform-then-aggregate (narrowing ConvMean) and both GEMM precisions
     agree with the aggregate-first fp32 path within 1e-5 (bar 1e-4)."""
