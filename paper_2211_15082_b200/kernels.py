@@ -427,6 +427,10 @@ def hot_indices(dg, row_bytes, reserve=0):
         dg._cache[("hot_requests", rows)] = seen + 1
         if seen < 1:
             return None
+        # the copy is outside the batch budget: only with ample free HBM
+        free, _total = torch.cuda.mem_get_info(dg.indices.device)
+        if free < 4 * dg.indices.numel() * dg.indices.element_size():
+            return None
         idx = dg.indices
         cnt = torch.bincount(idx.long(), minlength=int(dg.num_nodes))
         hot = torch.zeros(int(dg.num_nodes), dtype=torch.bool, device=idx.device)
