@@ -638,8 +638,12 @@ class LayerwiseEngine:
         lo, hi = 0, len(targets_np)
         if self.row_range is not None and full:
             lo, hi = self.row_range
+        # pinned + non_blocking: a pageable copy would block the host until the
+        # previous layer's kernels finish, and this block's host planning would
+        # then leave the device idle (cfg4 JKNet: 7 ms per call)
         targets_dev = None if full else torch.from_numpy(
-            np.ascontiguousarray(targets_np, dtype=np.int64)).to(self.dev)
+            np.ascontiguousarray(targets_np, dtype=np.int64)).pin_memory().to(
+                self.dev, non_blocking=True)
 
         # output stores
         if full:
