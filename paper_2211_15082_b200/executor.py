@@ -135,7 +135,8 @@ def _expand_dev(dg, nodes_np):
     dg.wait_rows()
     ids = kernels.IdSet(dg.num_nodes, dg.indptr.device)
     if len(nodes_np):
-        t = torch.from_numpy(np.ascontiguousarray(nodes_np, dtype=np.int64)).to(dg.indptr.device)
+        a = np.ascontiguousarray(nodes_np, dtype=np.int64)
+        t = torch.from_numpy(a if a.flags.writeable else a.copy()).to(dg.indptr.device)
         ids.add_ids(t).add_neighbors(dg, t)
     ids.finalize()
     return ids.extract().cpu().numpy()
@@ -641,7 +642,7 @@ class LayerwiseEngine:
         # pinned + non_blocking: a pageable copy would block the host until the
         # previous layer's kernels finish, and this block's host planning would
         # then leave the device idle (cfg4 JKNet: 7 ms per call)
-        targets_dev = None if full else torch.from_numpy(
+        targets_dev = None if full else torch.tensor(
             np.ascontiguousarray(targets_np, dtype=np.int64)).pin_memory().to(
                 self.dev, non_blocking=True)
 
