@@ -106,7 +106,9 @@ int glint_abi_version(void);
 #define GLINT_TUNE_GAT_L2 14      /* K4 cp.async ring L2 policy: 0 (default) source scores
                                      evict_last + Z rows evict_first, 1 none (results
                                      never change) */
-#define GLINT_TUNE_COUNT 15
+#define GLINT_TUNE_SAMPLE_SORT 15 /* glint_sample_neighbors: 0 warp top-k selection for
+                                     fanout <= 32, 1 the segmented-sort pipeline (same draws) */
+#define GLINT_TUNE_COUNT 16
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of
@@ -362,7 +364,10 @@ int glint_narrow_ids(int64_t n, const int64_t* src, int32_t* dst,
  * slot) and writes the kept source ids ascending to
  * out_indices[out_off[i] .. out_off[i+1]).  local_off[i] = sum of deg over
  * selected nodes before i (n_sel+1 entries, e_sel = local_off[n_sel]).
- * All arrays device memory; scratch from glint_sample_workspace_bytes. */
+ * All arrays device memory.  fanout <= 32 runs one warp per node (top-k by
+ * warp bitonic merges) and needs neither local_off nor a workspace (both may
+ * be NULL); larger fanouts segment-sort every slot and need local_off and
+ * glint_sample_workspace_bytes of scratch. */
 size_t glint_sample_workspace_bytes(int64_t n_sel, int64_t e_sel, int64_t e_out);
 int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices,
                            const int64_t* nodes, int64_t n_sel,

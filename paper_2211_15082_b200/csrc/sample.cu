@@ -62,6 +62,101 @@ __global__ void keep_kernel(int64_t n_sel, const int64_t* __restrict__ local_off
   for (int64_t j = lane; j < cnt; j += 32) kept[dst + j] = sorted[src + j];
 }
 
+// ---- fanout <= 32: one warp per node selects its fanout smallest (prio, slot)
+// keys with warp bitonic sorts -- no segmented sort of every edge --
+// then sorts the kept sources ascending.  Same draws and order as the sort
+// pipeline below (ties by slot, as numpy's stable lexsort).
+struct Cand {
+  uint64_t prio;
+  uint32_t slot;
+  int32_t src;
+};
+
+__device__ __forceinline__ bool less(const Cand& a, const Cand& b) {
+  return a.prio < b.prio || (a.prio == b.prio && a.slot < b.slot);
+}
+
+__device__ __forceinline__ Cand shfl_xor(const Cand& c, int m) {
+  Cand o;
+  o.prio = __shfl_xor_sync(0xffffffffu, c.prio, m);
+  o.slot = __shfl_xor_sync(0xffffffffu, c.slot, m);
+  o.src = __shfl_xor_sync(0xffffffffu, c.src, m);
+  return o;
+}
+
+// compare-exchange with the lane `m` away: the lower lane keeps the smaller
+// element iff `up`
+__device__ __forceinline__ void cmpx(Cand& c, int lane, int m, bool up) {
+  const Cand o = shfl_xor(c, m);
+  const bool lower = (lane & m) == 0;
+  const bool take_min = lower == up;
+  const bool o_less = less(o, c);
+  if (take_min ? o_less : less(c, o)) c = o;
+}
+
+__device__ __forceinline__ void bitonic_sort32(Cand& c, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int m = k >> 1; m > 0; m >>= 1) cmpx(c, lane, m, (lane & k) == 0 || k == 32);
+}
+
+// c: a bitonic sequence across the warp -> ascending
+__device__ __forceinline__ void bitonic_merge32(Cand& c, int lane) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) cmpx(c, lane, m, true);
+}
+
+__global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
+                              const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                              const int64_t* __restrict__ out_off, uint64_t base, int fanout,
+                              int32_t* __restrict__ out) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_sel) return;
+  const int64_t v = nodes ? nodes[w] : w;
+  const int64_t beg = indptr[v];
+  const int64_t deg = indptr[v + 1] - beg;
+  const int64_t dst = out_off[w];
+  const uint64_t hv = base ^ mix64(static_cast<uint64_t>(v) * kM1);
+  const Cand none{~0ull, 0xffffffffu, 0x7fffffff};
+  Cand best = none;
+  if (deg > fanout) {
+    for (int64_t c0 = 0; c0 < deg; c0 += 32) {
+      const int64_t sl = c0 + lane;
+      Cand c = none;
+      if (sl < deg) {
+        c.prio = mix64(hv ^ static_cast<uint64_t>(sl));
+        c.slot = static_cast<uint32_t>(sl);
+        c.src = __ldg(indices + beg + sl);
+      }
+      bitonic_sort32(c, lane);
+      // the 32 smallest of best (ascending) and c (ascending): min against the
+      // reversed chunk gives a bitonic sequence holding them
+      Cand r;
+      r.prio = __shfl_sync(0xffffffffu, c.prio, 31 - lane);
+      r.slot = __shfl_sync(0xffffffffu, c.slot, 31 - lane);
+      r.src = __shfl_sync(0xffffffffu, c.src, 31 - lane);
+      if (less(r, best)) best = r;
+      bitonic_merge32(best, lane);
+    }
+  } else if (lane < deg) {
+    best.prio = 0;
+    best.slot = static_cast<uint32_t>(lane);
+    best.src = __ldg(indices + beg + lane);
+  }
+  // the kept sources (lanes < min(fanout, deg)) ascending by id
+  const int keep = static_cast<int>(deg < fanout ? deg : fanout);
+  Cand k = none;
+  if (lane < keep) {
+    k.prio = static_cast<uint64_t>(static_cast<uint32_t>(best.src));
+    k.slot = 0;
+    k.src = best.src;
+  }
+  bitonic_sort32(k, lane);
+  if (lane < keep) out[dst + lane] = k.src;
+}
+
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 struct SampleWs {
@@ -113,13 +208,21 @@ int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices, const 
   GLINT_REQUIRE(e_sel < (1LL << 31) && n_sel < (1LL << 31),
                 "sample_neighbors: more than 2^31 edges or nodes per call");
   if (n_sel == 0 || e_sel == 0) return GLINT_OK;
-  GLINT_REQUIRE(indptr && indices && local_off && out_off && out_indices && workspace,
-                "sample_neighbors: null argument");
+  GLINT_REQUIRE(indptr && indices && out_off && out_indices, "sample_neighbors: null argument");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t base0 = mix64(mix64(static_cast<uint64_t>(seed)) ^
+                               mix64(static_cast<uint64_t>(static_cast<int64_t>(layer)) * kM2));
+  if (fanout <= 32 && tuning(GLINT_TUNE_SAMPLE_SORT) == 0) {   // no workspace, no local_off
+    const int64_t blocks = ceil_div(n_sel * 32, 256);
+    select_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n_sel, nodes, indptr, indices,
+                                                               out_off, base0, fanout, out_indices);
+    return launch_status("sample_select");
+  }
+  GLINT_REQUIRE(local_off && workspace, "sample_neighbors: null argument");
   SampleWs ws{};
   int rc = sample_ws(n_sel, e_sel, e_out, &ws);
   if (rc) return rc;
   GLINT_REQUIRE(workspace_bytes >= ws.total, "sample_neighbors: workspace too small");
-  cudaStream_t s = as_stream(stream);
   uint8_t* p = static_cast<uint8_t*>(workspace);
   uint64_t* keys_in = reinterpret_cast<uint64_t*>(p);
   uint64_t* keys_out = keys_in + e_sel;
@@ -127,8 +230,7 @@ int glint_sample_neighbors(const int64_t* indptr, const int32_t* indices, const 
   int32_t* vals_out = vals_in + e_sel;
   int32_t* kept = reinterpret_cast<int32_t*>(p + ws.keys + ws.vals);
   void* temp = p + ws.keys + ws.vals + ws.kept;
-  const uint64_t base = mix64(mix64(static_cast<uint64_t>(seed)) ^
-                              mix64(static_cast<uint64_t>(static_cast<int64_t>(layer)) * kM2));
+  const uint64_t base = base0;
   const int64_t blocks = ceil_div(n_sel * 32, 256);
   prio_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n_sel, nodes, indptr, indices,
                                                              local_off, base, keys_in, vals_in);

@@ -91,12 +91,12 @@ def sample_neighbors(g, nodes, fanout, seed, layer):
         raise ValueError(f"fanout must be >= 1, got {fanout}")
     if isinstance(g, DeviceGraph):
         # device draws (glint_sample_neighbors): same priorities, same bytes
-        nodes = np.unique(np.asarray(nodes, dtype=np.int64))
+        nodes = _sorted_unique(nodes)
         every = len(nodes) == g.num_nodes
         return kernels.sample_neighbors_dev(g, None if every else nodes, fanout, seed, layer)
     indptr_h, indices_h = _host_arrays(g)
     n = g.num_nodes
-    nodes = np.unique(np.asarray(nodes, dtype=np.int64))
+    nodes = _sorted_unique(nodes)
     out_ptr = np.zeros(n + 1, dtype=np.int64)
     if len(nodes) == 0:
         return CscGraph(n, 0, out_ptr, np.zeros(0, dtype=np.int64))

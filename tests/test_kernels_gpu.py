@@ -692,3 +692,26 @@ def test_k1_hot_row_l2_steering_same_bytes(cuda, monkeypatch):
     kernels.spmm_mean_hot(got, h, g, g.num_nodes, schedule=sched, n_hub=int(nh.item()))
     assert torch.equal(got, want)
     assert kernels.hot_indices(g, 48 * 4) is None        # narrow rows: no steering
+
+
+def test_sampling_select_path_equals_sort_path(cuda):
+    """fanout <= 32 selects each node's draws with warp bitonic merges; the
+    segmented-sort pipeline (GLINT_TUNE_SAMPLE_SORT = 1, and every fanout > 32)
+    gives the same sampled graph, for every node and for a node subset, on a
+    graph with hub rows and duplicate edges."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels, synth
+
+    g = synth.gen_products_like(30_000, 30_000 * 15, seed=4, device="cuda")
+    sub = np.sort(np.random.default_rng(1).choice(g.num_nodes, 5000, replace=False))
+    for nodes in (None, sub):
+        for fanout in (1, 10, 32):
+            a = kernels.sample_neighbors_dev(g, nodes, fanout, 7, 2)
+            _lib.call("glint_set_tuning", 15, 1)
+            try:
+                b = kernels.sample_neighbors_dev(g, nodes, fanout, 7, 2)
+            finally:
+                _lib.call("glint_set_tuning", 15, 0)
+            assert np.array_equal(a.indptr_host, b.indptr_host)
+            assert torch.equal(a.indices, b.indices), (fanout, nodes is None)

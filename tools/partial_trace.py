@@ -1,7 +1,8 @@
 """Device/host timeline and kernel summary of one cfg4 partial call (JKNet or
 APPNP, 10% targets, Products-shaped graph) -- where a partial call's time goes.
+`gcn3-sampling` traces a sampling-mode call (fanout 10, all nodes) of the cfg2 GCN.
 
-    python tools/partial_trace.py [jknet3|appnp3] > profiles/r02_cfg4_trace.jsonl
+    python tools/partial_trace.py [jknet3|appnp3|gcn3-sampling] > profiles/r02_cfg4_trace.jsonl
 """
 import json
 import pathlib
@@ -22,13 +23,18 @@ def main():
     g = synth.gen_products_like(n, und, seed=0, device="cuda")
     x = synth.gen_features_device(n, 100, seed=0, device="cuda")
     targets = np.sort(np.random.default_rng(0).choice(n, n // 10, replace=False)).astype(np.int64)
-    m = (synth.build_jknet(100, 256, 47, 3, seed=0) if name == "jknet3"
-         else synth.build_appnp(100, 256, 47, k=3, alpha=0.1, seed=0))
+    if name == "gcn3-sampling":
+        m = synth.build_gcn(100, 256, 47, 3, seed=0)
+        kw = dict(mode="sampling", fanout=10, seed=1)
+    else:
+        m = (synth.build_jknet(100, 256, 47, 3, seed=0) if name == "jknet3"
+             else synth.build_appnp(100, 256, 47, k=3, alpha=0.1, seed=0))
+        kw = dict(mode="partial", targets=targets)
     for rep in range(3):
         probe = KernelProbe()
         torch.cuda.synchronize()
-        res = run_inference(m, g, x, mode="partial", targets=targets, budget="device",
-                            output="device", reassociate=True, probe=probe)
+        res = run_inference(m, g, x, budget="device", output="device", reassociate=True,
+                            probe=probe, **kw)
         torch.cuda.synchronize()
         probe.mark("end")
         torch.cuda.synchronize()
