@@ -1702,14 +1702,25 @@ def _gather_rows(store: DeviceStore, row_ids, wanted, device):
             kernels.copy_rows(out, store.view(),
                               src_rows=torch.from_numpy(np.ascontiguousarray(wanted)).to(device))
         return out
-    pos = np.searchsorted(row_ids, wanted)
-    if len(wanted):
-        safe = np.minimum(pos, len(row_ids) - 1)
-        if not np.array_equal(row_ids[safe], wanted):
-            raise InternalError("output rows do not cover the requested targets")
     out = torch.empty((len(wanted), store.dim), dtype=torch.float32, device=device)
-    if len(wanted):
-        kernels.copy_rows(out, store.view(), src_rows=torch.from_numpy(pos.astype(np.int64)).to(device))
+    if not len(wanted):
+        return out
+    if store.rank_map is not None and store.rows is not None:
+        # positions on the device through the store's node -> row rank map
+        w = torch.tensor(np.ascontiguousarray(wanted, dtype=np.int64)).to(device)
+        if int(w.min()) < 0 or int(w.max()) >= store.rank_map.numel():
+            raise InternalError("output rows do not cover the requested targets")
+        pos = store.rank_map.index_select(0, w).to(torch.int64)
+        ok = (pos >= 0) & (pos < store.num_rows)
+        if not bool(ok.all()) or not torch.equal(store.rows.index_select(0, pos.clamp(0)), w):
+            raise InternalError("output rows do not cover the requested targets")
+        kernels.copy_rows(out, store.view(), src_rows=pos)
+        return out
+    pos = np.searchsorted(row_ids, wanted)
+    safe = np.minimum(pos, len(row_ids) - 1)
+    if not np.array_equal(row_ids[safe], wanted):
+        raise InternalError("output rows do not cover the requested targets")
+    kernels.copy_rows(out, store.view(), src_rows=torch.from_numpy(pos.astype(np.int64)).to(device))
     return out
 
 

@@ -187,9 +187,14 @@ def rcmk(g) -> NodeOrder:
     from .storage import DeviceGraph
 
     if isinstance(g, DeviceGraph) and int(g.num_nodes) > 0:
+        # a pure function of the (immutable) graph: computed once per DeviceGraph
+        hit = g._cache.get("rcmk_order")
+        if hit is not None:
+            return hit
         perm = _rcmk_device(g)
         if perm is not None:
-            return NodeOrder(perm)
+            order = g._cache["rcmk_order"] = NodeOrder(perm)
+            return order
         ptr, adj, _ = _sorted_adjacency_device(g)      # deep BFS: the host's queue
         ptr, adj = ptr.cpu().numpy(), adj.cpu().numpy()
         n = int(g.num_nodes)
@@ -268,16 +273,22 @@ def apply_order_device(g, x, order: NodeOrder):
     if order.is_identity():
         return dg, x
     dev = dg.indptr.device
-    perm = torch.from_numpy(order.perm).to(dev)
-    inv = torch.from_numpy(order.inv).to(dev)
-    new_indptr = kernels.degree_prefix_dev(dg, perm)
-    new_indices = torch.empty_like(dg.indices)
-    _lib.call("glint_relabel_csc", dg.num_nodes, kernels.ptr(dg.indptr), kernels.ptr(dg.indices),
-              kernels.ptr(perm), kernels.ptr(inv), kernels.ptr(new_indptr),
-              kernels.ptr(new_indices), kernels.stream_handle())
-    host_ptr = np.zeros(dg.num_nodes + 1, dtype=np.int64)
-    np.cumsum(np.diff(dg.indptr_host)[order.perm], out=host_ptr[1:])
-    g2 = DeviceGraph(dg.num_nodes, dg.num_edges, new_indptr, new_indices, host_ptr)
+    hit = dg._cache.get("relabelled")
+    if hit is not None and hit[0] is order:       # same graph, same order: same CSC
+        perm, g2 = hit[1], hit[2]
+    else:
+        perm = torch.from_numpy(order.perm).to(dev)
+        inv = torch.from_numpy(order.inv).to(dev)
+        new_indptr = kernels.degree_prefix_dev(dg, perm)
+        new_indices = torch.empty_like(dg.indices)
+        _lib.call("glint_relabel_csc", dg.num_nodes, kernels.ptr(dg.indptr),
+                  kernels.ptr(dg.indices), kernels.ptr(perm), kernels.ptr(inv),
+                  kernels.ptr(new_indptr), kernels.ptr(new_indices), kernels.stream_handle())
+        host_ptr = np.zeros(dg.num_nodes + 1, dtype=np.int64)
+        np.cumsum(np.diff(dg.indptr_host)[order.perm], out=host_ptr[1:])
+        g2 = DeviceGraph(dg.num_nodes, dg.num_edges, new_indptr, new_indices, host_ptr)
+        if dg is g:               # a caller's DeviceGraph (not a fresh upload): keep it
+            dg._cache["relabelled"] = (order, perm, g2)
     if x is None:
         return g2, None
     if isinstance(x, DeviceStore):
