@@ -198,7 +198,10 @@ int glint_gat_project_f32(int64_t M, int32_t heads, int32_t head_dim, int32_t he
   const int N = heads * head_pitch;
   GLINT_REQUIRE(lda >= K && ldw >= K && ldz >= N, "gat_project: leading dimension too small");
   cudaStream_t s = as_stream(stream);
-  if (precision == GLINT_PREC_3XTF32) {
+  // GLINT_TUNE_GAT_PROJ: 0 scores in the GEMM epilogue, 1 GEMM then the score
+  // kernel, 2 the latter for short K (< 192) only
+  const int split = tuning(GLINT_TUNE_GAT_PROJ);
+  if (precision == GLINT_PREC_3XTF32 && split != 1 && !(split == 2 && K < 192)) {
     const int rc = launch_gat_project_3xtf32(M, heads, head_dim, head_pitch, K, A, lda, a_rows,
                                              W_pad, ldw, attn, Z, ldz, s_src, s_dst, s);
     if (rc != GLINT_EUNSUPPORTED) return rc;
