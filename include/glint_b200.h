@@ -110,7 +110,9 @@ int glint_abi_version(void);
                                      fanout <= 32, 1 the segmented-sort pipeline (same draws) */
 #define GLINT_TUNE_GAT_PROJ 16   /* glint_gat_project_f32: 0 scores in the GEMM epilogue,
                                      1 GEMM + glint_gat_scores_f32, 2 the latter for K < 192 */
-#define GLINT_TUNE_COUNT 17
+#define GLINT_TUNE_PACK24_LOOP 17 /* e2e CSR packing on host threads: 0 eight ids per
+                                      three 64-bit stores, 1 the per-id loop (A/B) */
+#define GLINT_TUNE_COUNT 18
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of
