@@ -47,7 +47,6 @@ def main():
 
     import bench
     from paper_2211_15082_b200 import _lib, kernels
-    from paper_2211_15082_b200.storage import pitch_of
 
     dev = torch.device("cuda", 0)
     n, und = bench.sizes(argparse.Namespace(nodes=None, undirected=None))
