@@ -73,6 +73,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-parity", action="store_true")
     p.add_argument("--no-secondary", action="store_true")
+    p.add_argument("--no-cfg5", action="store_true", help="skip the 1.6B-edge cfg5 secondary")
     p.add_argument("--cpu-sample", type=int, default=None, help="target nodes per layer")
     p.add_argument("--tune", action="append", default=[],
                    help="diagnostics: glint_set_tuning KEY=VALUE (performance knobs only)")
@@ -776,6 +777,17 @@ def main():
         torch.cuda.empty_cache()
         sec[f"{'cfg2' if args.model == 'gcn3' else 'cfg3'}_rcmk"] = order_secondary(
             args, m, g, xt, world, local, agg_of[args.model])
+        # the other BASELINE configs, measured in the same driver run; a failure
+        # here is recorded, never allowed to lose the headline line
+        for key, fn in (("cfg4", lambda: cfg4_secondary(g, xt)),
+                        ("cfg5", lambda: None if args.no_cfg5 else cfg5_secondary())):
+            try:
+                r = fn()
+                if r is not None:
+                    sec[key] = r
+            except Exception as exc:  # noqa: BLE001
+                sec[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = args.cpu_sample or 4096       # per worker: ~16 workers x 1.5 s of CPU work
@@ -814,6 +826,62 @@ def order_secondary(args, m, g, xt, world, local, agg_name):
     del run, gi, xi
     torch.cuda.empty_cache()
     return out
+
+
+def cfg4_secondary(g, xt, reps=3):
+    """BASELINE configs[3]: JKNet and APPNP partial inference on a 10% target
+    subset of the same graph, through run_inference with device-resident inputs
+    (median of `reps` calls after one warm-up), each checked byte-for-byte
+    against the same rows of a full-mode run (row invariance)."""
+    import torch
+
+    from paper_2211_15082_b200 import synth
+    from paper_2211_15082_b200.executor import run_inference
+
+    n = g.num_nodes
+    targets = np.sort(np.random.default_rng(0).choice(n, n // 10, replace=False)).astype(np.int64)
+    out = {"workload": "cfg4 JKNet / APPNP (100->256->256->47) partial inference, 10% targets",
+           "targets": len(targets)}
+    for name, m in (("jknet3", synth.build_jknet(100, 256, 47, 3, seed=0)),
+                    ("appnp3", synth.build_appnp(100, 256, 47, k=3, alpha=0.1, seed=0))):
+        kw = dict(budget="device", output="device", reassociate=True)
+        want = run_inference(m, g, xt, **kw).output[torch.from_numpy(targets).cuda()]
+        run_inference(m, g, xt, mode="partial", targets=targets, **kw)
+        torch.cuda.synchronize()
+        times, res = [], None
+        for _ in range(reps):
+            res = None
+            t0 = time.perf_counter()
+            res = run_inference(m, g, xt, mode="partial", targets=targets, **kw)
+            torch.cuda.synchronize()
+            times.append(1e3 * (time.perf_counter() - t0))
+        ms = float(np.median(times))
+        out[name] = {"ms_per_call": round(ms, 3), "targets_per_s": len(targets) / (ms / 1e3),
+                     "all_ms": [round(t, 3) for t in times],
+                     "bit_identical_to_full_rows": bool(torch.equal(res.output, want)),
+                     "layer_batches": res.stats.layer_batches}
+        del want, res
+        torch.cuda.empty_cache()
+    return out
+
+
+def cfg5_secondary(steps=2, warmup=1, capacity_gib=16.0):
+    """BASELINE configs[4] on ONE B200 (tools/bench_papers.py): a 111M-node,
+    1.6B-edge Papers100M-shaped graph, 3-layer GCN 128->128->128->172, full
+    inference at a 16 GiB batch capacity, the engine owning (and freeing) x."""
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    import bench_papers
+
+    torch.cuda.empty_cache()
+    res = bench_papers.run(steps=steps, warmup=warmup, capacity_gib=capacity_gib)
+    torch.cuda.empty_cache()
+    return {k: res[k] for k in ("workload", "nodes", "in_edges", "value", "unit", "ms_per_step",
+                                "aggregation", "gemm", "capacity_gib")} | {
+        "step_ms": [round(st["ms"], 1) for st in res["per_step"]],
+        "layer_batches": res["per_step"][-1]["layer_batches"],
+        "peak_alloc_gib": round(res["per_step"][-1]["peak_alloc_gib"], 1)}
 
 
 if __name__ == "__main__":

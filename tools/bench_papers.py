@@ -30,7 +30,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def main():
+def run(nodes=None, steps=2, warmup=1, capacity_gib=16.0):
+    """The cfg5 measurement as a dict (bench.py's cfg5 secondary calls this)."""
     import numpy as np
     import torch
 
@@ -41,16 +42,9 @@ def main():
                                                 _as_device_store, annotate)
     from paper_2211_15082_b200.splitter import split
 
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--nodes", type=int, default=synth.PAPERS_NODES)
-    ap.add_argument("--steps", type=int, default=2)
-    ap.add_argument("--warmup", type=int, default=1)
-    ap.add_argument("--capacity-gib", type=float, default=16.0,
-                    help="batch footprint capacity (the batch controller's budget)")
-    args = ap.parse_args()
     _lib.load()
     dev = torch.device("cuda", 0)
-    n = args.nodes
+    n = nodes or synth.PAPERS_NODES
     und = int(round(n * synth.PAPERS_EDGES / 2 / synth.PAPERS_NODES))
     t0 = time.perf_counter()
     g = synth.gen_products_like(n, und, seed=0, device="cuda")
@@ -60,11 +54,11 @@ def main():
     m = synth.build_gcn(128, 128, 172, 3, seed=0)
     schedule = split(m)
     tsets = annotate(g, np.arange(0), m.depth, "full")
-    budget = DeviceBudget(int(args.capacity_gib * (1 << 30)))
+    budget = DeviceBudget(int(capacity_gib * (1 << 30)))
     th0 = Thresholds(1024, 32768)
-    steps = []
+    per_step = []
     summ = None
-    for i in range(args.warmup + args.steps):
+    for i in range(warmup + steps):
         x = _as_device_store(synth.gen_features_device(n, 128, seed=i, device="cuda"), dev)
         torch.cuda.synchronize()
         torch.cuda.reset_peak_memory_stats()
@@ -80,34 +74,51 @@ def main():
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e)
-        if i >= args.warmup:
+        if i >= warmup:
             summ = probe.summary()
-            steps.append({"ms": ms, "layers": [(nm, round(t, 2)) for nm, t in probe.timeline()],
-                          "batches": stats.batches, "layer_batches": stats.layer_batches,
-                          "peak_alloc_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
+            per_step.append({"ms": ms, "layers": [(nm, round(t, 2)) for nm, t in probe.timeline()],
+                             "batches": stats.batches, "layer_batches": stats.layer_batches,
+                             "peak_alloc_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
         del out, eng
         torch.cuda.empty_cache()
-    ms = float(np.mean([st["ms"] for st in steps]))
+    n_edges = int(g.num_edges)
+    del g
+    torch.cuda.empty_cache()
+    ms = float(np.mean([st["ms"] for st in per_step]))
     per = [summ.get(k, (0, 0, 0.0)) for k in ("spmm_mean", "conv_mean")]
     cnt, nbytes, agg_ms = (sum(v[i] for v in per) for i in range(3))
     lin = summ.get("linear", (0, 0, 0.0))
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    print(json.dumps({
+    return {
         "workload": "cfg5 3-layer GCN (ConvMean 128->128->128->172, ReLU) full inference, "
                     "OGBN-Papers100M-shaped graph, 1 B200",
-        "nodes": n, "in_edges": g.num_edges, "graph_gen_s": round(gen_s, 1),
-        "value": n / (ms / 1e3), "unit": "nodes/s", "ms_per_step": ms, "steps": args.steps,
-        "warmup": args.warmup,
+        "nodes": n, "in_edges": n_edges,
+        "graph_gen_s": round(gen_s, 1),
+        "value": n / (ms / 1e3), "unit": "nodes/s", "ms_per_step": ms, "steps": steps,
+        "warmup": warmup,
         "aggregation": {"kernels": {k: v for k, v in summ.items() if k != "linear"},
                         "launches": cnt, "algorithmic_bytes": nbytes, "ms": agg_ms,
                         "achieved_gbs": nbytes / (agg_ms / 1e3) / 1e9 if agg_ms else None,
                         "frac_of_peak": (nbytes / (agg_ms / 1e3) / 1e9 / peak) if agg_ms else None,
                         "peak_gbs": peak},
         "gemm": {"ms": lin[2], "tflops": lin[1] / (lin[2] / 1e3) / 1e12 if lin[2] else None},
-        "capacity_gib": args.capacity_gib, "per_step": steps,
-        "data": "synthetic (device generator, random-init weights)"}), flush=True)
+        "capacity_gib": capacity_gib, "per_step": per_step,
+        "data": "synthetic (device generator, random-init weights)"}
+
+
+def main():
+    from paper_2211_15082_b200 import synth
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nodes", type=int, default=synth.PAPERS_NODES)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--capacity-gib", type=float, default=16.0,
+                    help="batch footprint capacity (the batch controller's budget)")
+    args = ap.parse_args()
+    print(json.dumps(run(args.nodes, args.steps, args.warmup, args.capacity_gib)), flush=True)
 
 
 if __name__ == "__main__":
