@@ -780,7 +780,7 @@ def main():
         # the other BASELINE configs, measured in the same driver run; a failure
         # here is recorded, never allowed to lose the headline line
         for key, fn in (("cfg4", lambda: cfg4_secondary(g, xt)),
-                        ("cfg5", lambda: None if args.no_cfg5 else cfg5_secondary())):
+                        ("cfg5", lambda: None if (args.no_cfg5 or args.nodes) else cfg5_secondary())):
             try:
                 r = fn()
                 if r is not None:
