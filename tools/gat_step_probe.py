@@ -1,5 +1,5 @@
-"""Per-launch K4 times inside the cfg3 step for several hub thresholds
-(kernels.GAT_HUB_MIN_DEGREE), interleaved in one process."""
+"""Per-launch K4 times inside the cfg3 step, interleaved in one process, for
+K4 launch variants (GLINT_TUNE_GAT_VARIANT, `--variants 0,5,6`)."""
 import argparse
 import json
 import pathlib
@@ -21,10 +21,13 @@ def main():
     g, x = bench.device_inputs(n, und, 100, dev)
     run = bench.Runner(bench.build_model("gat3"), g, x, 1, 0)
     run.step()
+    from paper_2211_15082_b200 import _lib
+
+    variants = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,5,6,7,8,9").split(",")]
     res = {}
     for rep in range(4):
-        for t in (512, 4096):
-            kernels.GAT_HUB_MIN_DEGREE = t
+        for t in variants:
+            _lib.call("glint_set_tuning", 3, t)
             pr = KernelProbe()
             torch.cuda.synchronize()
             run.step(pr)
@@ -33,7 +36,7 @@ def main():
                 res.setdefault(t, []).append([round(ms, 3) for nm, _, ms in pr.launches()
                                               if nm == "gat_aggregate"])
     for t, v in res.items():
-        print(json.dumps({"gat_hub_min": t, "k4_ms_per_layer": np.median(np.asarray(v), axis=0).round(3).tolist(),
+        print(json.dumps({"gat_variant": t, "k4_ms_per_layer": np.median(np.asarray(v), axis=0).round(3).tolist(),
                           "all": v}))
 
 
