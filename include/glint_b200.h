@@ -112,7 +112,10 @@ int glint_abi_version(void);
                                      1 GEMM + glint_gat_scores_f32, 2 the latter for K < 192 */
 #define GLINT_TUNE_PACK24_LOOP 17 /* e2e CSR packing on host threads: 0 eight ids per
                                       three 64-bit stores, 1 the per-id loop (A/B) */
-#define GLINT_TUNE_COUNT 18
+#define GLINT_TUNE_GAT_PEAK_FIRST 18 /* K4 ring rows: 0 (default) the first ring slots of
+                                        Z rows are issued before the per-head peak pass,
+                                        1 peak pass first (A/B; results never change) */
+#define GLINT_TUNE_COUNT 19
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of

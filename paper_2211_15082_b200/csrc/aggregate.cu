@@ -1004,6 +1004,7 @@ struct GatArgs {
   float* __restrict__ wself;
   int64_t w_base;
   int l2_hint;   // source scores evict_last, Z rows evict_first (GLINT_TUNE_GAT_L2 = 1: off)
+  int z_first;   // ring prologue before the peak pass (GLINT_TUNE_GAT_PEAK_FIRST = 1: after)
 };
 
 __device__ __forceinline__ float gat_epilogue(const GatArgs& a, float v) {
@@ -1287,7 +1288,10 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
   }
 
   float sdst[H], peak[H];
-  {
+  // pass 1 (per-head peak); run before or after the ring prologue (a.z_first):
+  // the prologue's Z rows do not depend on it, so issuing them first overlaps
+  // their latency with the peak pass's dependent score loads
+  auto peak_pass = [&]() {
     const Scores<H> sd = load_scores<H>(a.s_dst + self * H, vec);
     const Scores<H> ss = load_scores<H>(a.s_src + self * H, vec);
 #pragma unroll
@@ -1315,7 +1319,8 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
       for (int o = LPR / 2; o > 0; o >>= 1)
         peak[h] = fmaxf(peak[h], __shfl_xor_sync(gmask, peak[h], o, LPR));
     }
-  }
+  };
+  if (!a.z_first) peak_pass();
   bool ok[VPL];
   int hk[VPL];
 #pragma unroll
@@ -1377,6 +1382,7 @@ __device__ __forceinline__ void gat_row_async(const GatArgs& a, int64_t r, int l
     if (ie < deg) issue(t);
     cp_async_commit();
   }
+  if (a.z_first) peak_pass();
   int slot = 0, jc = 0;
   for (int j = 0; j < deg; ++j) {
     if (jc == 0) {   // consumption enters a chunk: its weights from the staged scores
@@ -2127,6 +2133,7 @@ int glint_gat_aggregate_ws_f32(int64_t n_rows, int32_t heads, int32_t head_dim, 
   GatArgs a{};
   a.ra = RowAddr{indptr, indices, row_ids, row_base, self_rows, col_map};
   a.l2_hint = tuning(GLINT_TUNE_GAT_L2) == 0;   // default on: cfg3 step 71.1 -> 68.3 ms
+  a.z_first = tuning(GLINT_TUNE_GAT_PEAK_FIRST) == 0;
   a.heads = heads;
   a.head_dim = head_dim;
   a.head_pitch = head_pitch;

@@ -265,6 +265,15 @@ def test_gat_hub_paths_and_act_bit_identical(cuda, heads, dh):
         assert torch.equal(nopol, outs[0])
     finally:
         _lib.call("glint_set_tuning", 14, 0)
+    # the peak pass before the ring prologue (the pre-round-2 order): same bytes
+    _lib.call("glint_set_tuning", 18, 1)
+    try:
+        first = torch.empty_like(outs[0])
+        kernels.gat_aggregate(first, Z, s_src, s_dst, heads, dh, indptr, indices, n,
+                              schedule=sched, n_hub=int(nh.item()))
+        assert torch.equal(first, outs[0])
+    finally:
+        _lib.call("glint_set_tuning", 18, 0)
     # and the same bytes without any hub path (every row in the regular kernel),
     # for every launch variant (register-staged and cp.async ring)
     try:
