@@ -30,7 +30,7 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def run(nodes=None, steps=2, warmup=1, capacity_gib=16.0):
+def run(nodes=None, steps=2, warmup=1, capacity_gib=64.0, keep_cache=True):
     """The cfg5 measurement as a dict (bench.py's cfg5 secondary calls this)."""
     import numpy as np
     import torch
@@ -80,7 +80,8 @@ def run(nodes=None, steps=2, warmup=1, capacity_gib=16.0):
                              "batches": stats.batches, "layer_batches": stats.layer_batches,
                              "peak_alloc_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
         del out, eng
-        torch.cuda.empty_cache()
+        if not keep_cache:
+            torch.cuda.empty_cache()
     n_edges = int(g.num_edges)
     del g
     torch.cuda.empty_cache()
@@ -105,6 +106,8 @@ def run(nodes=None, steps=2, warmup=1, capacity_gib=16.0):
                         "peak_gbs": peak},
         "gemm": {"ms": lin[2], "tflops": lin[1] / (lin[2] / 1e3) / 1e12 if lin[2] else None},
         "capacity_gib": capacity_gib, "per_step": per_step,
+        "allocator": ("caching allocator kept between steps (steady state)" if keep_cache
+                      else "empty_cache between steps (every step allocates its stores)"),
         "data": "synthetic (device generator, random-init weights)"}
 
 
@@ -115,10 +118,14 @@ def main():
     ap.add_argument("--nodes", type=int, default=synth.PAPERS_NODES)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
-    ap.add_argument("--capacity-gib", type=float, default=16.0,
+    ap.add_argument("--capacity-gib", type=float, default=64.0,
                     help="batch footprint capacity (the batch controller's budget)")
+    ap.add_argument("--empty-cache", action="store_true",
+                    help="release the caching allocator's blocks between steps, so every "
+                         "step pays cudaMalloc of its 57-76 GB stores (tools/cfg5_cache_ab.sh)")
     args = ap.parse_args()
-    print(json.dumps(run(args.nodes, args.steps, args.warmup, args.capacity_gib)), flush=True)
+    print(json.dumps(run(args.nodes, args.steps, args.warmup, args.capacity_gib, not args.empty_cache)),
+          flush=True)
 
 
 if __name__ == "__main__":
