@@ -115,7 +115,11 @@ int glint_abi_version(void);
 #define GLINT_TUNE_GAT_PEAK_FIRST 18 /* K4 ring rows: 0 (default) the first ring slots of
                                         Z rows are issued before the per-head peak pass,
                                         1 peak pass first (A/B; results never change) */
-#define GLINT_TUNE_COUNT 19
+#define GLINT_TUNE_FUSED_PIPE 19  /* K7 gather warps: 0 (default) the next row claimed and
+                                      its indptr, first ids and self row loaded while the
+                                      current row's edges fly, 1 one row at a time (A/B;
+                                      results never change) */
+#define GLINT_TUNE_COUNT 20
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of

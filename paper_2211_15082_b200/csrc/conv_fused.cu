@@ -201,6 +201,7 @@ struct FArgs {
   int ring_off, stg_off, epi_off, bias_off;
   int64_t num_tiles;
   int max_ctas;                        // persistent CTAs (0: one per SM)
+  int pipe;                            // 1: next row prepared ahead (gather_rows_pipelined)
   int* __restrict__ tile_ctr;          // zeroed before the launch
   unsigned long long* __restrict__ prof;   // optional phase counters (diagnostics)
 };
@@ -258,6 +259,130 @@ __device__ __forceinline__ float4 gather_mean_row(const FArgs& a, int64_t r, int
   const float4 s = ldg_f4(a.h + self * a.ld_h + lane * 4);
   return make_float4(__fdiv_rn(__fadd_rn(acc.x, s.x), degp1), __fdiv_rn(__fadd_rn(acc.y, s.y), degp1),
                      __fdiv_rn(__fadd_rn(acc.z, s.z), degp1), __fdiv_rn(__fadd_rn(acc.w, s.w), degp1));
+}
+
+// A gather warp's claimed row (warp-uniform).
+struct GRow {
+  int seq, slot;
+  bool term;        // the tile counter ran out: no more tiles
+  bool valid;       // a row of a real tile (false: padding past n_rows)
+  int64_t beg;
+  int deg;
+  int32_t cur, nxt; // this lane's ids of the row's first two 32-edge chunks
+  float4 self_v;    // this lane's 4 columns of the self row
+};
+
+// The gather warps' loop with the next row prepared ahead: right after a row's
+// ring prologue is issued, the warp claims the next row and loads its
+// schedule slot, indptr pair, first ids and self row -- a chain of dependent
+// loads that now overlaps the current row's in-flight edges instead of
+// stalling an empty ring at every row start.  The per-edge loop is K1's
+// (gather_mean_row): one fp32 add chain per column in stored edge order, self
+// last, then the division -- byte-identical.  Terminal handling and the
+// staging hand-off are the per-row loop's.
+template <int R, int GT, bool MAP>
+__device__ __forceinline__ void gather_rows_pipelined(
+    const FArgs& a, int lane, bool ok, uint32_t ring_s, const float4* ring, float* stg,
+    int* row_ctr, int* tile_of, int* tile_flag, uint64_t* a_full, uint64_t* stg_empty,
+    unsigned long long& t_stg, unsigned long long& n_rows_done, unsigned long long& n_tiles) {
+  const char* hbase = reinterpret_cast<const char*>(a.h + lane * 4);
+  const int32_t ldb = static_cast<int32_t>(a.ld_h * 4);
+  auto prepare = [&](GRow& q) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(row_ctr, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    q.seq = t >> 7;
+    q.slot = t & (ROWS - 1);
+    const int tq = q.seq & 3;
+    if (q.slot == 0 && lane == 0) {
+      const int tid = atomicAdd(a.tile_ctr, 1);
+      tile_of[tq] = tid < a.num_tiles ? tid : -1;
+      st_release(&tile_flag[tq], q.seq + 1);
+    }
+    if (lane == 0)
+      while (ld_acquire(&tile_flag[tq]) != q.seq + 1) __nanosleep(32);
+    __syncwarp();
+    const int tid = *reinterpret_cast<volatile int*>(&tile_of[tq]);
+    q.term = tid < 0;
+    const int64_t idx = static_cast<int64_t>(tid) * ROWS + q.slot;
+    q.valid = !q.term && idx < a.n_rows;
+    q.beg = 0;
+    q.deg = 0;
+    q.cur = q.nxt = 0;
+    q.self_v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.prof && q.slot == 0 && !q.term) ++n_tiles;
+    if (!q.valid) return;
+    const int64_t r = a.schedule ? static_cast<int64_t>(a.schedule[idx]) : idx;
+    const int64_t rid = a.row_ids ? a.row_ids[r] : a.row_base + r;
+    q.beg = a.indptr[rid];
+    q.deg = static_cast<int>(a.indptr[rid + 1] - q.beg);
+    int64_t self = a.self_rows ? a.self_rows[r] : (rid & 0x7fffffff);
+    if (!a.self_rows && MAP) self = __ldg(a.col_map + self);
+    if (ok) q.self_v = ldg_f4(a.h + self * a.ld_h + lane * 4);
+    q.cur = (lane < q.deg) ? __ldg(a.indices + q.beg + lane) : 0;
+    q.nxt = (32 + lane < q.deg) ? __ldg(a.indices + q.beg + 32 + lane) : 0;
+  };
+
+  GRow C, N;
+  prepare(C);
+  while (true) {
+    if (C.term) {
+      // the slot-0 taker completes the terminal phase (after the previous
+      // tile's) so the converters and the MMA issuer see the end
+      if (C.slot == 0) {
+        if (C.seq > 0) mbar_wait(stg_empty, static_cast<uint32_t>(C.seq - 1) & 1u);
+        if (lane == 0) mbar_arrive_n(a_full, ROWS);
+      }
+      break;
+    }
+    const int deg = C.deg;
+    const int64_t beg = C.beg;
+    int ie = 0, cb = 0;
+    int32_t cur = C.cur, nxt = C.nxt;
+    auto issue = [&](int slot) {
+      if (ie - cb == 32) {
+        cb += 32;
+        cur = nxt;
+        nxt = (cb + 32 + lane < deg) ? __ldg(a.indices + beg + cb + 32 + lane) : 0;
+      }
+      int32_t id = __shfl_sync(0xffffffffu, cur, ie - cb) & 0x7fffffff;
+      if (MAP) id = __ldg(a.col_map + id);
+      if (ok) cp_async16(ring_s + static_cast<uint32_t>(slot * GT) * 16u, row_at(hbase, id, ldb));
+      ++ie;
+    };
+#pragma unroll
+    for (int g = 0; g < R; ++g) {
+      if (ie < deg) issue(g);
+      cp_async_commit();
+    }
+    prepare(N);   // the next row's dependent loads overlap this row's ring
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int base = 0;
+    for (int j = 0; j < deg; ++j) {
+      cp_async_wait<R - 1>();
+      if (ok) add4(acc, ring[base * GT]);
+      if (ie < deg) issue(base);
+      cp_async_commit();
+      base = (base + 1 == R) ? 0 : base + 1;
+    }
+    cp_async_wait<0>();
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (C.valid && ok) {
+      const float degp1 = static_cast<float>(deg + 1);
+      v = make_float4(__fdiv_rn(__fadd_rn(acc.x, C.self_v.x), degp1),
+                      __fdiv_rn(__fadd_rn(acc.y, C.self_v.y), degp1),
+                      __fdiv_rn(__fadd_rn(acc.z, C.self_v.z), degp1),
+                      __fdiv_rn(__fadd_rn(acc.w, C.self_v.w), degp1));
+    }
+    if (a.prof && C.valid) ++n_rows_done;
+    const unsigned long long ts = a.prof ? clock64() : 0;
+    if (C.seq > 0) mbar_wait(stg_empty, static_cast<uint32_t>(C.seq - 1) & 1u);
+    if (a.prof) t_stg += clock64() - ts;
+    if (C.valid && ok) *reinterpret_cast<float4*>(stg + C.slot * a.pitch + lane * 4) = v;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a_full);
+    C = N;
+  }
 }
 
 template <int ACT>
@@ -330,7 +455,11 @@ __global__ void __launch_bounds__(Roles<NG>::THREADS, 1) conv_mean_fused_kernel(
     const uint32_t ring_s = smem_addr(ring);
     unsigned long long t_loop = 0, t_stg = 0, t_tile = 0, n_rows_done = 0, n_tiles = 0;
     const unsigned long long t0 = a.prof ? clock64() : 0;
-    while (true) {
+    if (a.pipe)
+      gather_rows_pipelined<R, RL::GT, MAP>(a, lane, ok, ring_s, ring, stg, &row_ctr, tile_of,
+                                            tile_flag, &a_full, &stg_empty, t_stg, n_rows_done,
+                                            n_tiles);
+    while (!a.pipe) {
       int t = 0;
       if (lane == 0) t = atomicAdd(&row_ctr, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
@@ -682,6 +811,7 @@ extern "C" int glint_conv_mean_f32(int64_t n_rows, int32_t dim_in, int32_t dim_o
   a.nks = static_cast<int>(ceil_div(dim_in, fused::BK));
   a.pitch = fused::stage_pitch(dim_in);
   a.max_ctas = max_ctas;
+  a.pipe = tuning(GLINT_TUNE_FUSED_PIPE) == 0;   // row-ahead gather (0) or one row at a time (1)
   if (tuning(GLINT_TUNE_FUSED_PROF)) {
     void* p = nullptr;
     GLINT_CUDA(cudaGetSymbolAddress(&p, fused::g_fused_prof));

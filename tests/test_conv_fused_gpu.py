@@ -78,6 +78,13 @@ def test_conv_mean_equals_k1_k2_bytes(cuda, d_in, d_out, act, bias):
     g, w = got.cpu().numpy(), want.cpu().numpy()
     assert np.isfinite(g).all()
     assert g.tobytes() == w.tobytes(), rel_l2(g, w)
+    # the gather warps one row at a time (GLINT_TUNE_FUSED_PIPE = 1): same bytes
+    _lib.call("glint_set_tuning", 19, 1)
+    try:
+        kernels.conv_mean(got, h, Wt, bt, act, ip, ix, n, schedule=sched)
+        assert got.cpu().numpy().tobytes() == w.tobytes()
+    finally:
+        _lib.call("glint_set_tuning", 19, 0)
     # and against the oracle (numpy add.at mean + float64 transform)
     bc = orc.build_batch_csc(indptr, indices, np.arange(n))
     agg = orc.agg_mean(bc, x).astype(np.float64)
@@ -118,6 +125,12 @@ def test_conv_mean_natural_order_row_ids_and_col_map(cuda):
     got = torch.empty((B, d_out), dtype=torch.float32, device="cuda")
     kernels.conv_mean(got, h, Wt, bt, 1, ip, ix, B, row_ids=rid, col_map=cmap)
     assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    _lib.call("glint_set_tuning", 19, 1)
+    try:
+        kernels.conv_mean(got, h, Wt, bt, 1, ip, ix, B, row_ids=rid, col_map=cmap)
+        assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    finally:
+        _lib.call("glint_set_tuning", 19, 0)
     bc = orc.build_batch_csc(indptr, indices, targets)
     ref = np.maximum(orc.agg_mean(bc, x[bc.input_ids]).astype(np.float64) @ W.T.astype(np.float64)
                      + bv, 0.0)

@@ -25,7 +25,12 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-step", action="store_true")
     ap.add_argument("--variants", default="0", help="GLINT_TUNE_FUSED_VARIANT values (comma list)")
+    ap.add_argument("--knob", type=int, default=12,
+                    help="tuning knob --variants sweeps (12 FUSED_VARIANT, 19 FUSED_PIPE)")
     ap.add_argument("--shapes", default="100x256,128x256,128x128,100x47")
+    ap.add_argument("--graph", default="products", choices=("products", "papers"),
+                    help="papers: gen_products_like at cfg5's average degree (--nodes, "
+                         "default 20M), features 128-wide")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -37,8 +42,17 @@ def main():
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    n, und = bench.sizes(argparse.Namespace(nodes=args.nodes, undirected=None))
-    g, x100 = bench.device_inputs(n, und, 100, dev)
+    if args.graph == "papers":
+        from paper_2211_15082_b200 import synth
+
+        n = args.nodes or 20_000_000
+        und = int(round(n * synth.PAPERS_EDGES / 2 / synth.PAPERS_NODES))
+        g = synth.gen_products_like(n, und, seed=0, device="cuda")
+        x100 = torch.randn((n, 100), device=dev)
+        args.no_step = True
+    else:
+        n, und = bench.sizes(argparse.Namespace(nodes=args.nodes, undirected=None))
+        g, x100 = bench.device_inputs(n, und, 100, dev)
     E = g.num_edges
     sched, n_hub = kernels.degree_schedule(g.indptr, None, 0, n)
     n_hub = int(n_hub.item())
@@ -64,7 +78,7 @@ def main():
     print(json.dumps({"part": "schedule", "ms_sched_arange": tt,
                       "equal": bool(torch.equal(sc2, sched))}), flush=True)
     for (d_in, d_out), var in [(sh, int(v)) for sh in shapes for v in args.variants.split(",")]:
-        lib.glint_set_tuning(12, var)
+        lib.glint_set_tuning(args.knob, var)
         h = x100 if d_in == 100 else torch.randn((n, d_in), device=dev)
         W = torch.from_numpy((rng.normal(size=(d_out, d_in)) / np.sqrt(d_in)).astype(np.float32)).to(dev)
         b = torch.from_numpy(rng.normal(size=d_out).astype(np.float32)).to(dev)
@@ -101,7 +115,7 @@ def main():
                 "rows": int(cnt[3]), "tiles": int(cnt[4])}
         fb = conv_bytes(d_in, d_out, E, n)
         print(json.dumps({
-            "part": "layer", "variant": var, "d_in": d_in, "d_out": d_out, "nodes": n, "edges": E,
+            "part": "layer", "knob": args.knob, "variant": var, "d_in": d_in, "d_out": d_out, "nodes": n, "edges": E,
             "prof": prof,
             "unfused_ms": round(float(np.median(t_un)), 4), "k1_ms": round(float(np.median(t_k1)), 4),
             "fused_ms": round(float(np.median(t_fu)), 4),
@@ -113,7 +127,7 @@ def main():
         del agg, o1, o2
         torch.cuda.empty_cache()
 
-    lib.glint_set_tuning(12, 0)
+    lib.glint_set_tuning(args.knob, 0)
     if args.no_step:
         return
     m = bench.build_model("gcn3")
