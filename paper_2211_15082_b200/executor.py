@@ -489,11 +489,14 @@ class LayerwiseEngine:
         return pitch_of(w.shape[0]) < pitch_of(w.shape[1])
 
     def _fusions(self, blk):
-        """conv/linear op -> activation op fused into its GEMM epilogue."""
+        """conv/linear op -> activation op fused into its epilogue.  An identity
+        (DropoutIdentity: x at inference, reference kernels.py:206-231) fuses
+        the same way with no activation, so the producer writes straight into
+        the identity's destination (its store) instead of a copy pass."""
         fused = {}
         for o in blk.op_ids:
             k = blk.kinds[o]
-            if k not in ("ReLU", "LeakyReLU"):
+            if k not in _EPILOGUE_ACTS:
                 continue
             x = self.m.operators[o].inputs[0]
             if (x in blk.kinds and blk.kinds[x] in ("ConvMean", "ConvAttn", "Linear")
@@ -601,8 +604,7 @@ class LayerwiseEngine:
     def _eval_normal_into(self, out, op, operands, row_sel, fused_act=None):
         k = op.kind
         if k == "Linear":
-            act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
-                   "LeakyReLU": _lib.ACT_LEAKY_RELU}[fused_act]
+            act = _act_code(fused_act)
             kernels.linear_into(out, operands[0], self.params.w[op.op_id], self.params.b[op.op_id],
                                 act, a_rows=row_sel[0], precision=self.precision)
         elif k == "Concat":
@@ -669,7 +671,11 @@ class LayerwiseEngine:
             prefix = np.zeros(len(targets_np) + 1, dtype=np.int64)
         hub_pre, hub_host = (self._hub_counter(gl, targets_dev, full) if blk.has_conv
                              else (None, None))
+        if self.probe is not None:
+            self.probe.mark(f"L{layer} stores + hub prefix")
         layer_mats, layer_spaces = self._layer_inputs(blk, gl, targets_dev, full)
+        if self.probe is not None:
+            self.probe.mark(f"L{layer} input-domain ops")
         fused = self._fusions(blk)
         gat_cache = {}
         n_convs = sum(1 for _, k, _ in blk.iter_ops() if k in ("ConvMean", "ConvAttn"))
@@ -785,6 +791,8 @@ class LayerwiseEngine:
                     torch.cuda.empty_cache()
                     raise DeviceAllocationError(str(exc).splitlines()[0]) from exc
 
+        if self.probe is not None:
+            self.probe.mark(f"L{layer} transforms / whole layer")
         if full:
             self.plan_stream.wait_event(gl.indptr_event)     # planning reads only the CSR
         else:   # target lists / hub prefix were produced on the main stream
@@ -881,8 +889,7 @@ class LayerwiseEngine:
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, d_out)
-                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
-                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                act = _act_code(m.operators[act_op].kind if act_op else None)
                 if self.probe is not None:
                     self.probe.begin("spmm_mean")
                 kernels.spmm_mean(out, gat_cache[o], gl.indptr, gl.indices, B, row_ids=row_ids,
@@ -904,8 +911,7 @@ class LayerwiseEngine:
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, d_out)
-                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
-                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                act = _act_code(m.operators[act_op].kind if act_op else None)
                 if self.probe is not None:
                     self.probe.begin("conv_mean")
                 split = not self._fused_ok
@@ -936,8 +942,7 @@ class LayerwiseEngine:
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, m.out_dims[o])
-                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
-                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                act = _act_code(m.operators[act_op].kind if act_op else None)
                 if self.probe is not None:
                     self.probe.begin("linear")
                 kernels.linear_into(out, agg, self.params.w[o], self.params.b[o], act,
@@ -956,8 +961,7 @@ class LayerwiseEngine:
                 act_op = fused.get(o)
                 target = act_op or o
                 out = dest(target, H * dh)
-                act = {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU,
-                       "LeakyReLU": _lib.ACT_LEAKY_RELU}[m.operators[act_op].kind if act_op else None]
+                act = _act_code(m.operators[act_op].kind if act_op else None)
                 if self.probe is not None:
                     self.probe.begin("gat_aggregate")
                 hot = (kernels.hot_indices(gl, kernels.ld(Z) * 4, reserve=GAT_SCORE_L2)
@@ -1126,7 +1130,19 @@ class LayerwiseEngine:
             if exchange is not None:
                 exchange(self, blk)
             self.release_after(blk)
+            if self.probe is not None:
+                self.probe.mark(f"L{blk.layer} released")
         return self.stores[self.schedule.model_output.key]
+
+
+# ops a producer's epilogue absorbs: activations, and the inference identity
+_EPILOGUE_ACTS = ("ReLU", "LeakyReLU", "DropoutIdentity")
+
+
+def _act_code(kind):
+    """Epilogue activation code of a fused op kind (None: no fused op)."""
+    return {None: _lib.ACT_NONE, "ReLU": _lib.ACT_RELU, "LeakyReLU": _lib.ACT_LEAKY_RELU,
+            "DropoutIdentity": _lib.ACT_NONE}[kind]
 
 
 def agg_bytes(width, n_edges, n_rows, heads=0) -> int:
