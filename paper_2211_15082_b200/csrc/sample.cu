@@ -66,10 +66,16 @@ __global__ void keep_kernel(int64_t n_sel, const int64_t* __restrict__ local_off
 // keys with warp bitonic sorts -- no segmented sort of every edge --
 // then sorts the kept sources ascending.  Same draws and order as the sort
 // pipeline below (ties by slot, as numpy's stable lexsort).
+//   * A chunk of 32 slots is sorted and merged only if one of its keys beats
+//     the current fanout-th smallest (a warp ballot): past the first chunk
+//     most chunks of a long row are skipped outright.
+//   * Keys carry (prio, slot) only -- 3 shuffles per compare-exchange; the
+//     kept sources are loaded by slot at the end.
+//   * The kept sources are sorted by a 32-bit id bitonic (1 shuffle per
+//     step), skipped when they are ascending already (slices stored sorted).
 struct Cand {
   uint64_t prio;
   uint32_t slot;
-  int32_t src;
 };
 
 __device__ __forceinline__ bool less(const Cand& a, const Cand& b) {
@@ -80,7 +86,6 @@ __device__ __forceinline__ Cand shfl_xor(const Cand& c, int m) {
   Cand o;
   o.prio = __shfl_xor_sync(0xffffffffu, c.prio, m);
   o.slot = __shfl_xor_sync(0xffffffffu, c.slot, m);
-  o.src = __shfl_xor_sync(0xffffffffu, c.src, m);
   return o;
 }
 
@@ -107,6 +112,19 @@ __device__ __forceinline__ void bitonic_merge32(Cand& c, int lane) {
   for (int m = 16; m > 0; m >>= 1) cmpx(c, lane, m, true);
 }
 
+// ascending 32-bit ids across the warp (0x7fffffff pads the tail)
+__device__ __forceinline__ void bitonic_sort32_ids(int32_t& v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int m = k >> 1; m > 0; m >>= 1) {
+      const int32_t o = __shfl_xor_sync(0xffffffffu, v, m);
+      const bool up = (lane & k) == 0 || k == 32;
+      const bool take_min = ((lane & m) == 0) == up;
+      v = take_min ? min(v, o) : max(v, o);
+    }
+}
+
 __global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
                               const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                               const int64_t* __restrict__ out_off, uint64_t base, int fanout,
@@ -119,16 +137,24 @@ __global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
   const int64_t deg = indptr[v + 1] - beg;
   const int64_t dst = out_off[w];
   const uint64_t hv = base ^ mix64(static_cast<uint64_t>(v) * kM1);
-  const Cand none{~0ull, 0xffffffffu, 0x7fffffff};
-  Cand best = none;
+  const Cand none{~0ull, 0xffffffffu};
+  const int keep = static_cast<int>(deg < fanout ? deg : fanout);
+  int32_t id = 0x7fffffff;
   if (deg > fanout) {
+    Cand best = none;
     for (int64_t c0 = 0; c0 < deg; c0 += 32) {
       const int64_t sl = c0 + lane;
       Cand c = none;
       if (sl < deg) {
         c.prio = mix64(hv ^ static_cast<uint64_t>(sl));
         c.slot = static_cast<uint32_t>(sl);
-        c.src = __ldg(indices + beg + sl);
+      }
+      if (c0 > 0) {
+        // the current fanout-th smallest: a chunk with nothing below it is skipped
+        Cand kth;
+        kth.prio = __shfl_sync(0xffffffffu, best.prio, fanout - 1);
+        kth.slot = __shfl_sync(0xffffffffu, best.slot, fanout - 1);
+        if (__ballot_sync(0xffffffffu, less(c, kth)) == 0u) continue;
       }
       bitonic_sort32(c, lane);
       // the 32 smallest of best (ascending) and c (ascending): min against the
@@ -136,25 +162,18 @@ __global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
       Cand r;
       r.prio = __shfl_sync(0xffffffffu, c.prio, 31 - lane);
       r.slot = __shfl_sync(0xffffffffu, c.slot, 31 - lane);
-      r.src = __shfl_sync(0xffffffffu, c.src, 31 - lane);
       if (less(r, best)) best = r;
       bitonic_merge32(best, lane);
     }
+    if (lane < keep) id = __ldg(indices + beg + best.slot);
   } else if (lane < deg) {
-    best.prio = 0;
-    best.slot = static_cast<uint32_t>(lane);
-    best.src = __ldg(indices + beg + lane);
+    id = __ldg(indices + beg + lane);
   }
-  // the kept sources (lanes < min(fanout, deg)) ascending by id
-  const int keep = static_cast<int>(deg < fanout ? deg : fanout);
-  Cand k = none;
-  if (lane < keep) {
-    k.prio = static_cast<uint64_t>(static_cast<uint32_t>(best.src));
-    k.slot = 0;
-    k.src = best.src;
-  }
-  bitonic_sort32(k, lane);
-  if (lane < keep) out[dst + lane] = k.src;
+  // the kept sources (lanes < keep) ascending by id
+  const int32_t prev = __shfl_up_sync(0xffffffffu, id, 1);
+  if (__ballot_sync(0xffffffffu, lane > 0 && lane < keep && prev > id) != 0u)
+    bitonic_sort32_ids(id, lane);
+  if (lane < keep) out[dst + lane] = id;
 }
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
