@@ -74,6 +74,36 @@ def main():
                               "median": float(np.median(times[p]))}), flush=True)
         return
 
+    if "--knob-ab" in sys.argv:
+        # interleaved A/B of one tuning knob: --knob-ab 20=0,1
+        from paper_2211_15082_b200 import _lib
+        import numpy as np
+
+        spec = sys.argv[sys.argv.index("--knob-ab") + 1]
+        key, vals = spec.split("=")
+        vals = [int(v) for v in vals.split(",")]
+        times = {v: [] for v in vals}
+        res = None
+        for v in vals:
+            _lib.call("glint_set_tuning", int(key), v)
+            res = None
+            res = run_inference(m, hg, xh, budget=budget, output="numpy", reassociate=True)
+        for _ in range(8):
+            for v in vals:
+                _lib.call("glint_set_tuning", int(key), v)
+                res = None
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = run_inference(m, hg, xh, budget=budget, output="numpy", reassociate=True)
+                torch.cuda.synchronize()
+                times[v].append(1e3 * (time.perf_counter() - t0))
+        _lib.call("glint_set_tuning", int(key), 0)
+        for v in vals:
+            print(json.dumps({"model": model, "ab": f"tuning knob {key}", "value": v,
+                              "ms": [round(t, 1) for t in times[v]],
+                              "median": float(np.median(times[v]))}), flush=True)
+        return
+
     # --pack24-ab: alternate 24-bit packed and int32 CSR uploads in one process
     modes = (True, False) if "--pack24-ab" in sys.argv else (storage.PACK24,)
     times = {mode: [] for mode in modes}
