@@ -50,6 +50,51 @@ __global__ void ew_pointwise_kernel(EwArgs a) {
   }
 }
 
+// The pointwise kinds by rows and 16-byte chunks: LPR lanes per row, lane g
+// takes chunks g, g+LPR, ...  Used when every operand row and the output row
+// are 16-byte aligned with room for the last chunk (ld >= 4 ceil(dim/4)): the
+// last chunk may read pad columns, whose results are never stored.  Same
+// per-element arithmetic (and Add order) as ew_pointwise_kernel.
+__device__ __forceinline__ float ew_unary(int kind, float v) {
+  if (kind == GLINT_EW_RELU) return (v > 0.0f || v != v) ? v : 0.0f;
+  if (kind == GLINT_EW_LEAKY_RELU) return v >= 0.0f ? v : __fmul_rn(0.2f, v);
+  return v;
+}
+
+template <int LPR>
+__global__ void ew_rows_kernel(EwArgs a, int c4) {
+  constexpr int G = 32 / LPR;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = warp * G + lane / LPR;
+  if (i >= a.n_rows) return;
+  for (int c = lane % LPR; c < c4; c += LPR) {
+    const int col = 4 * c;
+    float4 v = ldg_f4(operand_row(a, 0, i) + col);
+    if (a.kind == GLINT_EW_ADD) {
+      for (int k = 1; k < a.n_in; ++k) {
+        const float4 w = ldg_f4(operand_row(a, k, i) + col);
+        v.x = __fadd_rn(v.x, w.x);
+        v.y = __fadd_rn(v.y, w.y);
+        v.z = __fadd_rn(v.z, w.z);
+        v.w = __fadd_rn(v.w, w.w);
+      }
+    } else {
+      v.x = ew_unary(a.kind, v.x);
+      v.y = ew_unary(a.kind, v.y);
+      v.z = ew_unary(a.kind, v.z);
+      v.w = ew_unary(a.kind, v.w);
+    }
+    float* o = a.out + i * a.ld_out + col;
+    if (col + 4 <= a.dim) {
+      *reinterpret_cast<float4*>(o) = v;
+    } else {
+      const float t[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; col + j < a.dim; ++j) o[j] = t[j];
+    }
+  }
+}
+
 // Norm: x / sqrt(sum(x*x) + 1e-12), one warp per row (kernels.py:227-230).
 __global__ void ew_norm_kernel(EwArgs a) {
   const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -123,9 +168,27 @@ int glint_elementwise_f32(int32_t kind, int64_t n_rows, int32_t dim, int32_t n_i
   if (kind == GLINT_EW_NORM) {
     ew_norm_kernel<<<static_cast<unsigned>(ceil_div(n_rows * 32, 256)), 256, 0, s>>>(a);
   } else {
-    const int64_t total = n_rows * dim;
-    const int64_t grid = std::min<int64_t>(ceil_div(total, 256), static_cast<int64_t>(sm_count()) * 16);
-    ew_pointwise_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(a);
+    const int c4 = static_cast<int>(ceil_div(dim, 4));
+    bool vec = ld_out % 4 == 0 && aligned16(out);
+    for (int k = 0; k < n_inputs; ++k)
+      vec = vec && a.ld[k] % 4 == 0 && a.ld[k] >= 4 * c4 && aligned16(a.in[k]);
+    if (vec) {
+      const int lpr = c4 <= 4 ? 4 : c4 <= 8 ? 8 : c4 <= 16 ? 16 : 32;
+      const int64_t grid = ceil_div(ceil_div(n_rows, 32 / lpr) * 32, 256);
+      if (grid > 0x7fffffffLL) {
+        set_error("elementwise: grid too large");
+        return GLINT_EINVAL;
+      }
+      const unsigned g = static_cast<unsigned>(grid);
+      if (lpr == 4) ew_rows_kernel<4><<<g, 256, 0, s>>>(a, c4);
+      else if (lpr == 8) ew_rows_kernel<8><<<g, 256, 0, s>>>(a, c4);
+      else if (lpr == 16) ew_rows_kernel<16><<<g, 256, 0, s>>>(a, c4);
+      else ew_rows_kernel<32><<<g, 256, 0, s>>>(a, c4);
+    } else {
+      const int64_t total = n_rows * dim;
+      const int64_t grid = std::min<int64_t>(ceil_div(total, 256), static_cast<int64_t>(sm_count()) * 16);
+      ew_pointwise_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(a);
+    }
   }
   return launch_status("elementwise");
 }

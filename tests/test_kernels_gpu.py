@@ -724,3 +724,57 @@ def test_sampling_select_path_equals_sort_path(cuda):
                 _lib.call("glint_set_tuning", 15, 0)
             assert np.array_equal(a.indptr_host, b.indptr_host)
             assert torch.equal(a.indices, b.indices), (fanout, nodes is None)
+
+
+@pytest.mark.parametrize("dim", [1, 3, 4, 5, 47, 48, 100, 130, 256])
+def test_elementwise_row_chunks_pitched_and_gathered(cuda, dim):
+    """K5 pointwise kinds on pitched stores (the 16-byte row-chunk kernel, whose
+    last chunk reads pad columns it never stores) and on unaligned views (the
+    per-element kernel), with row-gathered operands: bytes equal to numpy's
+    float32 arithmetic (reference kernels.py:206-231), pads untouched."""
+    import torch
+
+    from paper_2211_15082_b200 import kernels
+    from paper_2211_15082_b200.storage import pitch_of
+
+    rng = np.random.default_rng(dim)
+    n = 777
+    p = pitch_of(dim)
+
+    def padded(x, fill):
+        t = torch.full((x.shape[0], p + 4), fill, dtype=torch.float32, device="cuda")
+        t[:, :dim] = torch.from_numpy(x).cuda()
+        return t
+
+    xs = [rng.normal(size=(n, dim)).astype(np.float32) for _ in range(3)]
+    xs[0][::7, 0] = np.nan
+    xs[0][1::5, -1] = -0.0
+    sel = rng.integers(0, n, size=n)
+    for aligned in (True, False):
+        c0 = 0 if aligned else 1               # a 4-byte offset view: the per-element kernel
+        bufs = [padded(x, float("nan")) for x in xs]
+        ops = [b[:, c0:c0 + dim] if aligned else torch.roll(b, 1, 1)[:, c0:c0 + dim]
+               for b in bufs]
+        host = [o.cpu().numpy() for o in ops]
+        sel_t = torch.from_numpy(sel).cuda()
+        for kind in ("ReLU", "LeakyReLU", "DropoutIdentity", "Add"):
+            out_buf = torch.full((n, p + 4), 7.0, device="cuda")
+            out = out_buf[:, c0:c0 + dim]
+            if kind == "Add":
+                kernels.elementwise_into(out, kind, ops, [None, sel_t, None])
+                want = (host[0] + host[1][sel]) + host[2]
+            else:
+                kernels.elementwise_into(out, kind, ops[:1], None)
+                x = host[0]
+                want = {"ReLU": np.maximum(x, np.float32(0)),
+                        "LeakyReLU": np.where(x >= 0, x, np.float32(0.2) * x),
+                        "DropoutIdentity": x}[kind]
+            got = out_buf.cpu().numpy()
+            g, w = got[:, c0:c0 + dim], want.astype(np.float32)
+            # NaN kept where numpy keeps it (its payload is not part of the contract);
+            # every other element bit-equal (so -0.0 vs +0.0 counts)
+            assert (np.isnan(g) == np.isnan(w)).all(), (kind, aligned)
+            fin = ~np.isnan(w)
+            assert g[fin].tobytes() == w[fin].tobytes(), (kind, aligned)
+            # nothing outside the view was written
+            assert (got[:, :c0] == 7.0).all() and (got[:, c0 + dim:] == 7.0).all(), (kind, aligned)
