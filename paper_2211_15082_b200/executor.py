@@ -575,7 +575,20 @@ class LayerwiseEngine:
             rows = ids.extract()
             space = _RowSpace(rows, ids.rank_map())
             n_rows = int(rows.shape[0])
+        # an activation / identity whose producer is an input-domain Linear used
+        # only by it runs in that GEMM's epilogue (the producer's rows are never
+        # materialised), as _fusions does for the target domain
+        fused, skip = {}, set()
         for o in ops:
+            if blk.kinds[o] not in _EPILOGUE_ACTS:
+                continue
+            x = self.m.operators[o].inputs[0]
+            if (x in ops and blk.kinds[x] == "Linear" and self.users[x] == [o]
+                    and x not in blk.outputs):
+                fused[x], skip = o, skip | {o}
+        for o in ops:
+            if o in skip:
+                continue
             op = self.m.operators[o]
             operands, row_sel = [], []
             for p in op.inputs:
@@ -594,9 +607,15 @@ class LayerwiseEngine:
                         row_sel.append(sp.positions(sel))
             width = self.m.out_dims[o]
             out = torch.empty((n_rows, pitch_of(width)), dtype=torch.float32, device=self.dev)[:, :width]
-            self._eval_normal_into(out, op, operands, row_sel, fused_act=None)
-            mats[o] = out
-            spaces[o] = space
+            act_op = fused.get(o)
+            self._eval_normal_into(out, op, operands, row_sel,
+                                   fused_act=blk.kinds[act_op] if act_op else None)
+            target = act_op or o
+            mats[target] = out
+            spaces[target] = space
+            if act_op is None:
+                mats[o] = out
+                spaces[o] = space
         return mats, spaces
 
     # -- operator evaluation --------------------------------------------------
