@@ -1792,10 +1792,14 @@ int launch_linear_3xtf32(int64_t M, int N, int K, const float* A, int64_t lda,
     GLINT_CUDA(cudaGetSymbolAddress(&p, g_gemm_prof));
     a.prof = static_cast<unsigned long long*>(p);
   }
-  const bool vec = (lda % 4 == 0) && (ldw % 4 == 0) && (K % 4 == 0) && aligned16(A) && aligned16(W);
+  // 16-byte pitched rows: v3's tensor maps cover exactly K columns (the box
+  // beyond K is zero-filled by the TMA), so K need not be a multiple of 4 there;
+  // v2/v1's vector loads would read the pad columns, so they also need K % 4 == 0
+  const bool pitched = (lda % 4 == 0) && (ldw % 4 == 0) && aligned16(A) && aligned16(W);
+  const bool vec = pitched && (K % 4 == 0);
   // v3 (tensor-map TMA, CTA pairs / resident W), then v2 (row-gathered A),
   // unless the knobs ask for an older kernel
-  if (vec && tuning(GLINT_TUNE_GEMM_V1) == 0 && tuning(GLINT_TUNE_GEMM_V3) == 0) {
+  if (pitched && tuning(GLINT_TUNE_GEMM_V1) == 0 && tuning(GLINT_TUNE_GEMM_V3) == 0) {
     const int rc = v3::dispatch_v3<false>(a, act, s);
     if (rc != GLINT_EUNSUPPORTED) return rc;
   }

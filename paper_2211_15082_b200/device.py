@@ -53,19 +53,38 @@ class DeviceBudget:
         return cls(cap)
 
 
-def device_memory(device=None):
-    """(free, total) bytes of a CUDA device, as reported by the driver."""
+# cudaMemGetInfo costs ~1-2 ms per call on the B200 boxes and now and then tens
+# of ms (tools/partial_host_profile.py: one call of eight took ~45 ms), so a
+# query is reused for MEMINFO_TTL_S: in between, free HBM moves by what this
+# process's caching allocator reserved or released since the query.
+MEMINFO_TTL_S = 2.0
+_MEMINFO = {}
+
+
+def device_memory(device=None, max_age_s=None):
+    """(free, total) bytes of a CUDA device: the driver's numbers, at most
+    `max_age_s` (default MEMINFO_TTL_S) old, corrected for this process's
+    reservations since (torch.cuda.memory_reserved)."""
     import ctypes
+    import time
 
     import torch
 
     from . import _lib
 
     dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    ttl = MEMINFO_TTL_S if max_age_s is None else max_age_s
+    now = time.monotonic()
+    reserved = torch.cuda.memory_reserved(dev)
+    hit = _MEMINFO.get(dev)
+    if hit is not None and now - hit[0] <= ttl:
+        _t, free_q, total, reserved_q = hit
+        return max(0, free_q - (reserved - reserved_q)), total
     free = ctypes.c_size_t(0)
     total = ctypes.c_size_t(0)
     _lib.call("glint_device_info", int(dev), None, None, None,
               ctypes.addressof(free), ctypes.addressof(total))
+    _MEMINFO[dev] = (now, int(free.value), int(total.value), reserved)
     return int(free.value), int(total.value)
 
 

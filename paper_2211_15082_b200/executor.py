@@ -391,8 +391,13 @@ class _Params:
         self.w, self.b, self.attn, self.w_pad = {}, {}, {}, {}
         for op in m.operators.values():
             if op.kind in ("ConvMean", "Linear"):
-                self.w[op.op_id] = torch.from_numpy(np.ascontiguousarray(
-                    op.params["weight"], dtype=np.float32)).to(device)
+                # rows padded to a 16-byte pitch (K2's tensor maps need it; the
+                # pad is zero and never read)
+                w = np.ascontiguousarray(op.params["weight"], dtype=np.float32)
+                wp = torch.zeros((w.shape[0], pitch_of(w.shape[1])), dtype=torch.float32,
+                                 device=device)
+                wp[:, :w.shape[1]] = torch.from_numpy(w).to(device)
+                self.w[op.op_id] = wp[:, :w.shape[1]]
                 b = op.params.get("bias")
                 self.b[op.op_id] = (None if b is None else torch.from_numpy(
                     np.ascontiguousarray(b, dtype=np.float32)).to(device))
@@ -1617,6 +1622,8 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
     g_i, x_i = apply_order_device(dg0, x0, node_order)
     if mode == "full" or targets is None:
         internal = user_targets                      # sorted(inv[arange(N)]) == arange(N)
+    elif node_order.is_identity():
+        internal = _sorted_unique(user_targets)      # ids are distinct: a sorted copy
     else:
         internal = np.sort(node_order.inv[user_targets]) if len(user_targets) else user_targets
     thresholds = thresholds or Thresholds(n_t=1024, n_i=32768)

@@ -778,3 +778,45 @@ def test_elementwise_row_chunks_pitched_and_gathered(cuda, dim):
             assert g[fin].tobytes() == w[fin].tobytes(), (kind, aligned)
             # nothing outside the view was written
             assert (got[:, :c0] == 7.0).all() and (got[:, c0 + dim:] == 7.0).all(), (kind, aligned)
+
+
+@pytest.mark.parametrize("K,N", [(47, 47), (5, 16), (50, 100), (130, 47), (47, 256)])
+def test_linear_unaligned_k_pitched_rows(cuda, K, N):
+    """K2 with K % 4 != 0 on 16-byte pitched rows (v3's tensor maps zero-fill
+    the box beyond K): the same bytes as the v1 kernel and as the row-gathered
+    (a_rows) path, and within the 3xTF32 bar of fp64 (reference kernels.py:95-107)."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+    from paper_2211_15082_b200.storage import pitch_of
+
+    rng = np.random.default_rng(K * 1000 + N)
+    M = 3001
+    x = rng.normal(size=(M, K)).astype(np.float32)
+    w = (rng.normal(size=(N, K)) / np.sqrt(K)).astype(np.float32)
+    b = rng.normal(size=N).astype(np.float32)
+
+    def pitched(a, fill=float("nan")):
+        t = torch.full((a.shape[0], pitch_of(a.shape[1])), fill, dtype=torch.float32, device="cuda")
+        t[:, : a.shape[1]] = torch.from_numpy(a).cuda()
+        return t[:, : a.shape[1]]
+
+    xd, wd = pitched(x), pitched(w, 0.0)
+    bd = torch.from_numpy(b).cuda()
+
+    def run(**kw):
+        o = torch.empty((M, pitch_of(N)), device="cuda")[:, :N]
+        kernels.linear_into(o, xd, wd, bd, _lib.ACT_RELU, precision=_lib.PREC_3XTF32, **kw)
+        return o.cpu().numpy()
+
+    got = run()
+    _lib.call("glint_set_tuning", 4, 1)          # the v1 kernel
+    try:
+        v1 = run()
+    finally:
+        _lib.call("glint_set_tuning", 4, 0)
+    assert got.tobytes() == v1.tobytes()
+    rows = torch.arange(M, device="cuda", dtype=torch.int64)
+    assert run(a_rows=rows).tobytes() == got.tobytes()
+    ref = np.maximum(x.astype(np.float64) @ w.T.astype(np.float64) + b, 0.0)
+    assert rel_l2(got, ref) <= 5e-6
