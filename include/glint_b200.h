@@ -421,6 +421,13 @@ int glint_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t
                           int64_t row_bytes, int64_t rows, glint_stream_t stream);
 int glint_upload_query(void* handle, int32_t chunk);
 int glint_upload_finish(void* handle);
+/* Pageable host -> device copy of `bytes` through the library's pinned
+ * staging on `threads` CPU threads (each thread double-buffers its slice);
+ * returns once every byte has landed.  run_inference uses it for numpy
+ * feature matrices (reference API: storage.py / executor.py:481-543 take
+ * host arrays), which a plain pageable cudaMemcpy moves at ~10 GB/s. */
+int glint_h2d_pageable(void* dst_dev, const void* src_host, int64_t bytes, int32_t threads,
+                       glint_stream_t stream);
 /* Host int64 -> int32 narrowing on `threads` CPU threads (host pointers);
  * returns the number of ids outside int32 (the e2e upload narrows CSR chunks
  * on the host so they cross PCIe at half the bytes). */

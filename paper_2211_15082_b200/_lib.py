@@ -93,6 +93,7 @@ SIGNATURES = {
     "glint_copy_rows_async": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "glint_upload_query": (ctypes.c_int, [_P, _I32]),
     "glint_upload_finish": (ctypes.c_int, [_P]),
+    "glint_h2d_pageable": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
     "glint_sample_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "glint_sample_neighbors": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _I64, _I32, _I64,
                                               _I32, _P, _P, _SZ, _P]),
@@ -134,6 +135,7 @@ KERNELS_PER_CALL = {"glint_conv_mean_f32": 2, "glint_rcmk_components": 3, "glint
                     "glint_rcmk_sorted_host": 0, "glint_sample_neighbors": 4,
                     "glint_gat_aggregate_ws_f32": 2, "glint_upload_start": 0, "glint_upload_start_packed": 1, "glint_copy_rows_async": 0,
                     "glint_upload_wait": 0, "glint_upload_query": 0, "glint_upload_finish": 0,
+                    "glint_h2d_pageable": 0,
                     "glint_device_info": 0, "glint_set_tuning": 0, "glint_debug_counters": 0}
 LAUNCHES = [0]
 

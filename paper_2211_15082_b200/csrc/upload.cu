@@ -255,6 +255,80 @@ int glint_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t
   return GLINT_OK;
 }
 
+// Pageable host -> device copy through pinned staging on `threads` host
+// threads.  A plain cudaMemcpy from pageable memory goes through the driver's
+// own staging at ~10 GB/s (the reference API hands run_inference numpy
+// features); here thread t owns a contiguous slice of the source, copies it
+// in kStageChunk pieces into its two pinned halves (memcpy on the CPU) and
+// queues each piece's cudaMemcpyAsync, waiting for a half's previous copy
+// before refilling it.  The staging is allocated once per process (and grown
+// on demand) under a mutex that also serialises concurrent callers.  Returns
+// after every piece has landed (the synchronous semantics of the pageable copy).
+namespace {
+constexpr size_t kStageChunk = size_t{4} << 20;
+std::mutex g_stage_mu;
+uint8_t* g_stage = nullptr;
+size_t g_stage_bytes = 0;
+}  // namespace
+
+int glint_h2d_pageable(void* dst_dev, const void* src_host, int64_t bytes, int32_t threads,
+                       glint_stream_t stream) {
+  GLINT_REQUIRE(bytes >= 0 && threads >= 1, "h2d_pageable: bad argument");
+  if (bytes == 0) return GLINT_OK;
+  GLINT_REQUIRE(dst_dev && src_host, "h2d_pageable: null pointer");
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  const int t = static_cast<int>(std::min<int64_t>(
+      std::min(threads, 32), std::max<int64_t>(1, bytes / static_cast<int64_t>(kStageChunk))));
+  const size_t need = static_cast<size_t>(t) * 2 * kStageChunk;
+  if (g_stage_bytes < need) {
+    if (g_stage) cudaFreeHost(g_stage);
+    g_stage = nullptr;
+    g_stage_bytes = 0;
+    GLINT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_stage), need, cudaHostAllocDefault));
+    g_stage_bytes = need;
+  }
+  int dev = 0;
+  GLINT_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = as_stream(stream);
+  std::atomic<int> err{0};
+  auto work = [&](int k) {
+    cudaSetDevice(dev);
+    const int64_t lo = bytes * k / t, hi = bytes * (k + 1) / t;
+    uint8_t* half[2] = {g_stage + (2 * k) * kStageChunk, g_stage + (2 * k + 1) * kStageChunk};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool used[2] = {false, false};
+    for (int h = 0; h < 2; ++h)
+      if (cudaEventCreateWithFlags(&ev[h], cudaEventDisableTiming) != cudaSuccess) err = 1;
+    int h = 0;
+    for (int64_t off = lo; off < hi && !err; off += static_cast<int64_t>(kStageChunk)) {
+      const size_t len = static_cast<size_t>(std::min<int64_t>(kStageChunk, hi - off));
+      if (used[h] && cudaEventSynchronize(ev[h]) != cudaSuccess) err = 1;
+      std::memcpy(half[h], static_cast<const uint8_t*>(src_host) + off, len);
+      if (cudaMemcpyAsync(static_cast<uint8_t*>(dst_dev) + off, half[h], len,
+                          cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaEventRecord(ev[h], s) != cudaSuccess)
+        err = 1;
+      used[h] = true;
+      h ^= 1;
+    }
+    for (int q = 0; q < 2; ++q) {
+      if (ev[q]) {
+        if (used[q] && cudaEventSynchronize(ev[q]) != cudaSuccess) err = 1;
+        cudaEventDestroy(ev[q]);
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  if (err) {
+    set_error("h2d_pageable: CUDA copy failed");
+    return GLINT_ECUDA;
+  }
+  return GLINT_OK;
+}
+
 // Blocks until chunk k's copy is queued, then makes `stream` wait for it.
 int glint_upload_wait(void* handle, int32_t chunk, glint_stream_t stream) {
   auto* u = static_cast<Upload*>(handle);

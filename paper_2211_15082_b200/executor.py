@@ -1160,6 +1160,11 @@ class LayerwiseEngine:
 
 
 # ops a producer's epilogue absorbs: activations, and the inference identity
+# e2e chunking: CSRs below SMALL_UPLOAD_EDGES edges upload in one chunk; the
+# output streams to the host in chunks of about SINK_CHUNK_BYTES
+SMALL_UPLOAD_EDGES = 8 << 20
+SINK_CHUNK_BYTES = 57_500_000
+
 _EPILOGUE_ACTS = ("ReLU", "LeakyReLU", "DropoutIdentity")
 
 
@@ -1601,9 +1606,13 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
         # geometric 1/16, 1/8, 1/4, 1/2 plan, whose last half-of-the-edges chunk
         # left 7.7 ms of layer 1 behind the upload; 66.6 for 8 uniform chunks;
         # profiles/r01_e2e_fracs_ab.jsonl).  Without host narrowing: 16 chunks.
-        chunks = int(os.environ.get("GLINT_UPLOAD_CHUNKS", "5" if HOST_NARROW else "16"))
+        # A small CSR (cfg1: 2M edges) goes in one chunk: its upload is shorter
+        # than the per-chunk planning and launches it would overlap.
+        small = g.num_edges < SMALL_UPLOAD_EDGES
+        chunks = int(os.environ.get("GLINT_UPLOAD_CHUNKS",
+                                    "1" if small else ("5" if HOST_NARROW else "16")))
         geometric = os.environ.get("GLINT_UPLOAD_GEOMETRIC", "0") == "1"
-        fracs = ((0.0625, 0.25, 0.5, 0.75) if HOST_NARROW and not geometric
+        fracs = ((0.0625, 0.25, 0.5, 0.75) if HOST_NARROW and not geometric and not small
                  and "GLINT_UPLOAD_CHUNKS" not in os.environ else None)
         dg0 = DeviceGraph.upload_async(g, dev, copy, after_indptr=upload_features, chunks=chunks,
                                        geometric=geometric, fracs=fracs)
@@ -1647,11 +1656,13 @@ def run_inference(m: ModelGraph, g, x_store, *, mode="full", targets=None, fanou
             eng.sink = streamed
             if "GLINT_SINK_CHUNKS" not in os.environ:
                 # the device->host copy outlasts the last layer, so it should
-                # start early: ~128 MiB chunks, 8..16 of them (tools/e2e_ab.py
-                # --sink-ab: GCN 8 uniform chunks 63.6 ms vs 64.4 with 4;
-                # profiles/r01_e2e_sink_ab.jsonl)
+                # start early: chunks of ~57 MB, 1..16 of them -- GCN's 0.46 GB
+                # output in 8 (tools/e2e_ab.py --sink-ab: 63.6 ms vs 64.4 with
+                # 4; profiles/r01_e2e_sink_ab.jsonl), GAT's 1.84 GB in 16, and a
+                # small output in one piece (each chunk costs ~0.2 ms of host
+                # launches and planning)
                 out_bytes = g.num_nodes * m.output_dim * 4
-                eng.sink_chunks = int(min(16, max(8, round(out_bytes / (128 << 20)))))
+                eng.sink_chunks = int(min(16, max(1, round(out_bytes / SINK_CHUNK_BYTES))))
         eng.probe = probe
         store = eng.run(exchange=ex)
         if ex is not None:

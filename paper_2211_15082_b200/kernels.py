@@ -96,7 +96,20 @@ def to_device(x, dtype=None, device=None):
     if dtype is None:
         dtype = torch.float32 if arr.dtype.kind == "f" else torch.int64
     np_dtype = {torch.float32: np.float32, torch.int64: np.int64, torch.int32: np.int32}[dtype]
-    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dtype)).to(dev)
+    arr = np.ascontiguousarray(arr, dtype=np_dtype)
+    if arr.nbytes >= PAGEABLE_STAGED_MIN:
+        # large host arrays: the library's multi-threaded pinned staging
+        # (glint_h2d_pageable) instead of the driver's ~10 GB/s pageable path
+        out = torch.empty(arr.shape, dtype=dtype, device=dev)
+        _lib.call("glint_h2d_pageable", out.data_ptr(), arr.ctypes.data, arr.nbytes,
+                  PAGEABLE_THREADS, stream_handle())
+        return out
+    return torch.from_numpy(arr).to(dev)
+
+
+# numpy arrays at least this large go through glint_h2d_pageable
+PAGEABLE_STAGED_MIN = int(os.environ.get("GLINT_PAGEABLE_STAGED_MIN", 8 << 20))
+PAGEABLE_THREADS = int(os.environ.get("GLINT_PAGEABLE_THREADS", 8))
 
 
 def _f32(x):

@@ -820,3 +820,24 @@ def test_linear_unaligned_k_pitched_rows(cuda, K, N):
     assert run(a_rows=rows).tobytes() == got.tobytes()
     ref = np.maximum(x.astype(np.float64) @ w.T.astype(np.float64) + b, 0.0)
     assert rel_l2(got, ref) <= 5e-6
+
+
+@pytest.mark.parametrize("n_floats", [1, 1 << 20, (2 << 20) + 3, (13 << 20) + 1, 25_000_001])
+def test_h2d_pageable_bytes(cuda, n_floats):
+    """glint_h2d_pageable (pinned staging on host threads) lands the exact bytes
+    of a pageable numpy array, for sizes below, at and across its chunking."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(n_floats % 1000)
+    a = rng.normal(size=n_floats).astype(np.float32)
+    out = torch.empty(n_floats, dtype=torch.float32, device="cuda")
+    for threads in (1, 3, 8):
+        out.fill_(float("nan"))
+        _lib.call("glint_h2d_pageable", out.data_ptr(), a.ctypes.data, a.nbytes, threads,
+                  kernels.stream_handle())
+        assert out.cpu().numpy().tobytes() == a.tobytes(), threads
+    # and through to_device (the path run_inference takes for numpy features)
+    t = kernels.to_device(a.reshape(-1, 1) if n_floats % 4 else a.reshape(-1, 4))
+    assert t.cpu().numpy().tobytes() == a.tobytes()
