@@ -125,6 +125,64 @@ __device__ __forceinline__ void bitonic_sort32_ids(int32_t& v, int lane) {
     }
 }
 
+// 32-bit keys for rows of at most 64 slots: the top 32 bits of the priority
+// with the slot as tie-break (2 shuffles per compare-exchange).  Exact unless
+// a slot outside the kept set shares the top 32 bits of the fanout-th
+// smallest key -- checked by a ballot, and such a row (probability ~deg 2^-32)
+// takes the 64-bit path.
+struct Key32 {
+  uint32_t hi;
+  uint32_t slot;
+};
+
+__device__ __forceinline__ bool less32(const Key32& a, const Key32& b) {
+  return a.hi < b.hi || (a.hi == b.hi && a.slot < b.slot);
+}
+
+__device__ __forceinline__ void cmpx32(Key32& c, int lane, int m, bool up) {
+  Key32 o;
+  o.hi = __shfl_xor_sync(0xffffffffu, c.hi, m);
+  o.slot = __shfl_xor_sync(0xffffffffu, c.slot, m);
+  const bool take_min = ((lane & m) == 0) == up;
+  if (take_min ? less32(o, c) : less32(c, o)) c = o;
+}
+
+__device__ __forceinline__ void bitonic_sort32_k(Key32& c, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int m = k >> 1; m > 0; m >>= 1) cmpx32(c, lane, m, (lane & k) == 0 || k == 32);
+}
+
+// the fanout smallest of a row with deg <= 64 slots; false if not exact
+__device__ __forceinline__ bool select64(uint64_t hv, int64_t deg, int fanout, int lane,
+                                         uint32_t* slot_out) {
+  const Key32 none{0xffffffffu, 0xffffffffu};
+  Key32 a = none, b = none;
+  if (lane < deg) a = Key32{static_cast<uint32_t>(mix64(hv ^ static_cast<uint64_t>(lane)) >> 32),
+                            static_cast<uint32_t>(lane)};
+  if (lane + 32 < deg)
+    b = Key32{static_cast<uint32_t>(mix64(hv ^ static_cast<uint64_t>(lane + 32)) >> 32),
+              static_cast<uint32_t>(lane + 32)};
+  const Key32 a0 = a, b0 = b;
+  bitonic_sort32_k(a, lane);
+  if (deg > 32) {
+    bitonic_sort32_k(b, lane);
+    Key32 r;
+    r.hi = __shfl_sync(0xffffffffu, b.hi, 31 - lane);
+    r.slot = __shfl_sync(0xffffffffu, b.slot, 31 - lane);
+    if (less32(r, a)) a = r;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) cmpx32(a, lane, m, true);
+  }
+  const uint32_t t = __shfl_sync(0xffffffffu, a.hi, fanout - 1);
+  const int kept = __popc(__ballot_sync(0xffffffffu, lane < fanout && a.hi == t));
+  const int all = __popc(__ballot_sync(0xffffffffu, lane < deg && a0.hi == t)) +
+                  __popc(__ballot_sync(0xffffffffu, lane + 32 < deg && b0.hi == t));
+  *slot_out = a.slot;
+  return kept == all;
+}
+
 __global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
                               const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                               const int64_t* __restrict__ out_off, uint64_t base, int fanout,
@@ -140,7 +198,10 @@ __global__ void select_kernel(int64_t n_sel, const int64_t* __restrict__ nodes,
   const Cand none{~0ull, 0xffffffffu};
   const int keep = static_cast<int>(deg < fanout ? deg : fanout);
   int32_t id = 0x7fffffff;
-  if (deg > fanout) {
+  uint32_t slot64 = 0;
+  if (deg > fanout && deg <= 64 && select64(hv, deg, fanout, lane, &slot64)) {
+    if (lane < keep) id = __ldg(indices + beg + slot64);
+  } else if (deg > fanout) {
     Cand best = none;
     for (int64_t c0 = 0; c0 < deg; c0 += 32) {
       const int64_t sl = c0 + lane;
