@@ -119,7 +119,14 @@ int glint_abi_version(void);
                                       its indptr, first ids and self row loaded while the
                                       current row's edges fly, 1 one row at a time (A/B;
                                       results never change) */
-#define GLINT_TUNE_COUNT 20
+#define GLINT_TUNE_GAT_EPI 20     /* fused GAT score epilogue (K3): 0 (default) each
+                                      16-column half-chunk lies in one head (head pitch
+                                      % 16 == 0), a_src / a_dst as 128-bit loads, 32-column
+                                      chunks on v3 and v3 for every K; 1 the per-column head
+                                      walk in 16-column chunks, v2 for K < 192 (the earlier
+                                      default); 3 as 0 with 16-column chunks (A/B; results
+                                      never change); DIAGNOSTIC 2 no score math */
+#define GLINT_TUNE_COUNT 21
 int glint_set_tuning(int key, int value);
 int glint_get_tuning(int key);
 /* Copy (host_out, n <= 8) and optionally reset the phase-cycle counters of

@@ -156,6 +156,7 @@ struct TcArgs {
   float* s_src;              // [M, heads]
   float* s_dst;
   int heads, head_dim, head_pitch;
+  int sc_mode;               // GLINT_TUNE_GAT_EPI (0 chunked fast path, 1 per-column walk, 2 diagnostic)
   unsigned long long* prof;  // optional phase-cycle counters (GLINT_TUNE_GEMM_PROF)
 };
 
@@ -638,28 +639,63 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, uint32_t taddr, float
     // the head changes at warp-uniform positions (no per-element lookup or
     // divergence); each head's dot products stay one sequential fmaf chain.
     const int64_t row = row_base + lane;
-    int h = min(col0 / a.head_pitch, a.heads - 1);
-    int next = (h + 1) * a.head_pitch;      // first column of the following head
-    if (h != st.h) {
-      score_flush(a, st, row);
-      st.h = h;
-      st.ps = 0.0f;
-      st.pd = 0.0f;
-    }
+    if (a.sc_mode == 2) {
+      // diagnostic: no score math
+    } else if (a.sc_mode != 1 && a.head_pitch % 16 == 0 && col0 + CW <= a.N) {
+      // every 16-column half of the chunk lies in one head (chunks start at
+      // multiples of 16): no per-column head or bounds checks, a_src / a_dst
+      // as 128-bit broadcast loads; the same fmaf chain order, so the same bits
 #pragma unroll
-    for (int i = 0; i < CW; ++i) {
-      const int col = col0 + i;
-      if (col >= a.N) break;
-      if (col == next && h + 1 < a.heads) {
+      for (int hb = 0; hb < CW / 16; ++hb) {
+        const int cc = col0 + 16 * hb;
+        const int h = cc / a.head_pitch;
+        if (h != st.h) {
+          score_flush(a, st, row);
+          st.h = h;
+          st.ps = 0.0f;
+          st.pd = 0.0f;
+        }
+        const float4* ts = reinterpret_cast<const float4*>(sc_tab + cc);
+        const float4* td = reinterpret_cast<const float4*>(sc_tab + kScMaxN + cc);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 s4 = ts[q4];
+          const float4 d4 = td[q4];
+          const float* vv = v + 16 * hb + 4 * q4;
+          st.ps = fmaf(vv[0], s4.x, st.ps);
+          st.pd = fmaf(vv[0], d4.x, st.pd);
+          st.ps = fmaf(vv[1], s4.y, st.ps);
+          st.pd = fmaf(vv[1], d4.y, st.pd);
+          st.ps = fmaf(vv[2], s4.z, st.ps);
+          st.pd = fmaf(vv[2], d4.z, st.pd);
+          st.ps = fmaf(vv[3], s4.w, st.ps);
+          st.pd = fmaf(vv[3], d4.w, st.pd);
+        }
+      }
+    } else {
+      int h = min(col0 / a.head_pitch, a.heads - 1);
+      int next = (h + 1) * a.head_pitch;      // first column of the following head
+      if (h != st.h) {
         score_flush(a, st, row);
-        ++h;
-        next += a.head_pitch;
         st.h = h;
         st.ps = 0.0f;
         st.pd = 0.0f;
       }
-      st.ps = fmaf(v[i], sc_tab[col], st.ps);
-      st.pd = fmaf(v[i], sc_tab[kScMaxN + col], st.pd);
+#pragma unroll
+      for (int i = 0; i < CW; ++i) {
+        const int col = col0 + i;
+        if (col >= a.N) break;
+        if (col == next && h + 1 < a.heads) {
+          score_flush(a, st, row);
+          ++h;
+          next += a.head_pitch;
+          st.h = h;
+          st.ps = 0.0f;
+          st.pd = 0.0f;
+        }
+        st.ps = fmaf(v[i], sc_tab[col], st.ps);
+        st.pd = fmaf(v[i], sc_tab[kScMaxN + col], st.pd);
+      }
     }
   }
 #pragma unroll
@@ -1566,8 +1602,15 @@ gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const float* bias_g = bias_s;
       v2::ScoreAcc sa{-1, 0.0f, 0.0f};
       if constexpr (SC) {
+        int c0 = cbeg;
+        if (a.sc_mode == 0 || a.sc_mode == 2) {   // 32-column chunks (1, 3: 16)
 #pragma unroll 1
-        for (int c0 = cbeg; c0 + 16 <= cend; c0 += 16)
+          for (; c0 + 32 <= cend; c0 += 32)
+            v2::epi_chunk<32, ACT, SC>(a, tbase + c0, stage, bias_g + c0, has_bias, row_base,
+                                       n0 + c0, lane, sc_tab, sa);
+        }
+#pragma unroll 1
+        for (; c0 + 16 <= cend; c0 += 16)
           v2::epi_chunk<16, ACT, SC>(a, tbase + c0, stage, bias_g + c0, has_bias, row_base,
                                      n0 + c0, lane, sc_tab, sa);
         if (cend > cbeg) v2::score_flush(a, sa, row_base + lane);
@@ -1713,9 +1756,11 @@ int launch_v3_act(const TcArgs& a, int act, cudaStream_t s) {
 template <bool SC>
 int dispatch_v3(const TcArgs& a, int act, cudaStream_t s) {
   if (a.a_rows) return GLINT_EUNSUPPORTED;   // row-gathered A: no tensor map (v2 path)
-  // short-K score projections are epilogue-bound (per-row score chains); v2's
-  // 128-row tiles measured faster there (profiles/r02_gemm_v3.jsonl)
-  if (SC && a.K < 192) return GLINT_EUNSUPPORTED;
+  // with the per-column score walk (GLINT_TUNE_GAT_EPI 1) short-K score
+  // projections are epilogue-bound and v2's 128-row tiles were faster there;
+  // the chunked score path runs them on v3 (100 -> 4x64: 0.99 vs 1.75 ms,
+  // profiles/r02_gemm_sc_modes.jsonl)
+  if (SC && a.K < 192 && a.sc_mode == 1) return GLINT_EUNSUPPORTED;
   if (a.N <= 64 && a.K <= 512) {
     if (a.N <= 16) return launch_v3_act<16, SC, false, true>(a, act, s);
     if (a.N <= 32) return launch_v3_act<32, SC, false, true>(a, act, s);
@@ -1760,6 +1805,7 @@ int launch_gat_project_3xtf32(int64_t M, int heads, int head_dim, int head_pitch
   a.heads = heads;
   a.head_dim = head_dim;
   a.head_pitch = head_pitch;
+  a.sc_mode = tuning(GLINT_TUNE_GAT_EPI);
   if (tuning(GLINT_TUNE_GEMM_V3) == 0) {
     const int rc = v3::dispatch_v3<true>(a, GLINT_ACT_NONE, s);
     if (rc != GLINT_EUNSUPPORTED) return rc;

@@ -451,6 +451,39 @@ def test_tcgen05_v3_gat_project(cuda, M, heads, dh, K):
     assert rel_l2(sd.cpu().numpy(), wdst) <= 1e-5
 
 
+@pytest.mark.parametrize("M,heads,dh,K", [(1000, 4, 64, 100), (777, 4, 47, 256), (513, 4, 64, 256),
+                                          (300, 4, 10, 200), (65, 8, 32, 192)])
+def test_gat_score_epilogue_modes_same_bytes(cuda, M, heads, dh, K):
+    """The one-head half-chunk score path (GLINT_TUNE_GAT_EPI 0: 32-column
+    chunks, v3 for every K; 3: 16-column chunks) and the per-column head walk
+    (1: v2 for K < 192) give the same Z, s_src and s_dst bytes, on v3 and on v2
+    (GLINT_TUNE_GEMM_V3 1); head pitch 12 (dh 10) takes the per-column walk."""
+    import torch
+
+    from paper_2211_15082_b200 import _lib, kernels
+
+    rng = np.random.default_rng(7 * M + K)
+    xd = torch.from_numpy(rng.normal(size=(M, K)).astype(np.float32)).cuda()
+    w = (rng.normal(size=(heads, dh, K)) / np.sqrt(K)).astype(np.float32)
+    w_pad = kernels.padded_head_weight(torch.from_numpy(w).cuda())
+    att = torch.from_numpy(rng.normal(size=(heads, 2 * dh)).astype(np.float32)).cuda()
+    outs = {}
+    try:
+        for v3off in (0, 1):
+            for mode in (0, 1, 3):
+                _lib.call("glint_set_tuning", 9, v3off)
+                _lib.call("glint_set_tuning", 20, mode)
+                res = kernels.attn_project(xd, w_pad, att, heads, dh, precision=_lib.PREC_3XTF32)
+                torch.cuda.synchronize()
+                outs[(v3off, mode)] = [t.cpu().numpy().tobytes() for t in res]
+    finally:
+        _lib.call("glint_set_tuning", 9, 0)
+        _lib.call("glint_set_tuning", 20, 0)
+    base = outs[(0, 1)]
+    for key, got in outs.items():
+        assert got == base, key
+
+
 def test_shape_errors_are_value_errors(cuda):
     from paper_2211_15082_b200 import kernels
 

@@ -67,13 +67,17 @@ def main():
             want = xs @ wp.T
         outs = {}
         for kv in (int(v) for v in args.kernels.split(",")):
-            _lib.call("glint_set_tuning", 9, 1 if kv == 2 else 0)
+            _lib.call("glint_set_tuning", 9, 1 if kv == 2 else tune.get(9, 0))
             if kind == "s":
-                out = None
+                # outputs allocated once: a fresh 2.5 GB Z per call put cudaMalloc
+                # inside the timed reps (noisy, up to 10x)
+                pitch = kernels.head_pitch(hd)
+                out = (torch.empty((M, heads * pitch), device="cuda"),
+                       torch.empty((M, heads), device="cuda"), torch.empty((M, heads), device="cuda"))
 
                 def run():
-                    nonlocal out
-                    out = kernels.attn_project(x, w_pad, attn, heads, hd, precision=_lib.PREC_3XTF32)
+                    kernels.attn_project(x, w_pad, attn, heads, hd, precision=_lib.PREC_3XTF32,
+                                         out=out)
             else:
                 out = torch.empty((M, N), device="cuda")
 
@@ -114,7 +118,7 @@ def main():
             if kv != 3 and 3 in outs:
                 rec["bytes_equal_v3"] = bool(torch.equal(outs[3], z))
             print(json.dumps(rec), flush=True)
-        _lib.call("glint_set_tuning", 9, 0)
+        _lib.call("glint_set_tuning", 9, tune.get(9, 0))
         del x, w, outs
 
 
