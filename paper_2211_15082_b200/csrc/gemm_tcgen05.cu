@@ -567,7 +567,7 @@ struct Cfg2 {
   static constexpr int EPI_BYTES = kEpiWarps2 * 32 * EPI_LD * 4 + kEpiWarps2 * BN * 4;
   static constexpr int SC_OFF = EPI_OFF + EPI_BYTES;      // score tables (SC kernels only)
   static constexpr int SMEM = EPI_OFF + EPI_BYTES;
-  static constexpr int SMEM_SC = SC_OFF + 3 * kScMaxN * 4;
+  static constexpr int SMEM_SC = SC_OFF + 2 * kScMaxN * 4;   // a_src | a_dst
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (static_cast<uint32_t>(BN >> 3) << 17) |
                                     (static_cast<uint32_t>(HALF >> 4) << 24);
@@ -927,14 +927,13 @@ __global__ void __launch_bounds__(Roles<MH>::THREADS, 1) gemm_v2_kernel(TcArgs a
     const bool has_bias = a.bias != nullptr;
     float* sc_tab = reinterpret_cast<float*>(smem + C::SC_OFF);
     if constexpr (SC) {
-      // per-column a_src / a_dst / head tables, shared by the 8 epilogue warps
+      // per-column a_src / a_dst tables, shared by the 8 epilogue warps
       for (int c = threadIdx.x - Rl::EPI * 32; c < a.N; c += kEpiWarps2 * 32) {
         const int hh = c / a.head_pitch;
         const int j = c - hh * a.head_pitch;
         const bool live = hh < a.heads && j < a.head_dim;
         sc_tab[c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + j) : 0.0f;
         sc_tab[kScMaxN + c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + a.head_dim + j) : 0.0f;
-        sc_tab[2 * kScMaxN + c] = __int_as_float(min(hh, a.heads - 1));
       }
       asm volatile("bar.sync 2, %0;" ::"r"(kEpiWarps2 * 32) : "memory");
     }
@@ -1145,7 +1144,9 @@ struct Plan3 {
 // staging tiles + per-warp bias copies + score tables
 template <int BN, bool SC>
 constexpr int epi_bytes() {
-  return nepi<SC>() * (32 * EPI_LD + BN) * 4 + (SC ? 3 * v2::kScMaxN * 4 : 0);
+  // two score tables (a_src | a_dst): at BN = 256 this keeps the epilogue at 48 KB,
+  // so the score-fused pair kernel holds 3 operand stages like the plain one
+  return nepi<SC>() * (32 * EPI_LD + BN) * 4 + (SC ? 2 * v2::kScMaxN * 4 : 0);
 }
 
 template <int BN, bool PAIR, bool RESW, bool SC>
@@ -1571,7 +1572,6 @@ gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const bool live = hh < a.heads && j < a.head_dim;
         sc_tab[c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + j) : 0.0f;
         sc_tab[v2::kScMaxN + c] = live ? __ldg(a.attn + hh * 2 * a.head_dim + a.head_dim + j) : 0.0f;
-        sc_tab[2 * v2::kScMaxN + c] = __int_as_float(min(hh, a.heads - 1));
       }
       asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
     } else if constexpr (NEPI == 8) {
