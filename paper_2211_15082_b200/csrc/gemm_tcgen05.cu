@@ -1762,10 +1762,14 @@ int dispatch_v3(const TcArgs& a, int act, cudaStream_t s) {
   // profiles/r02_gemm_sc_modes.jsonl)
   if (SC && a.K < 192 && a.sc_mode == 1) return GLINT_EUNSUPPORTED;
   if (a.N <= 64 && a.K <= 512) {
-    if (a.N <= 16) return launch_v3_act<16, SC, false, true>(a, act, s);
-    if (a.N <= 32) return launch_v3_act<32, SC, false, true>(a, act, s);
-    if (a.N <= 48) return launch_v3_act<48, SC, false, true>(a, act, s);
-    return launch_v3_act<64, SC, false, true>(a, act, s);
+    // resident W: falls through to the pair kernel when W raw + lo leave
+    // fewer than 2 A stages of shared memory (e.g. N = 64, K = 512)
+    int rc;
+    if (a.N <= 16) rc = launch_v3_act<16, SC, false, true>(a, act, s);
+    else if (a.N <= 32) rc = launch_v3_act<32, SC, false, true>(a, act, s);
+    else if (a.N <= 48) rc = launch_v3_act<48, SC, false, true>(a, act, s);
+    else rc = launch_v3_act<64, SC, false, true>(a, act, s);
+    if (rc != GLINT_EUNSUPPORTED) return rc;
   }
   if (a.N <= 64) return launch_v3_act<64, SC, true, false>(a, act, s);
   if (a.N <= 128) return launch_v3_act<128, SC, true, false>(a, act, s);

@@ -387,7 +387,7 @@ def test_tcgen05_3xtf32_linear(cuda, M, N, K, act):
 @pytest.mark.parametrize("M,N,K", [(1, 47, 100), (300, 47, 256), (1000, 256, 256), (1000, 256, 100),
                                    (129, 300, 64), (257, 16, 3), (4096, 128, 128), (77, 48, 188),
                                    (5000, 256, 100), (513, 172, 128), (700, 65, 40), (300, 64, 600),
-                                   (2000, 600, 36), (33, 1, 9)])
+                                   (2000, 600, 36), (33, 1, 9), (600, 64, 512), (400, 48, 480)])
 @pytest.mark.parametrize("act", [0, 1])
 def test_tcgen05_v3_linear(cuda, M, N, K, act):
     """The v3 GEMM (tensor-map TMA, CTA pairs for N > 64, resident W for N <= 64)
