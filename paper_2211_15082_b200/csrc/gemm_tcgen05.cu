@@ -1108,10 +1108,13 @@ constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, W_EPI = W_CONV + NGRP * NCONV;
 // epilogue warps: 4 (one per TMEM lane quarter); the GAT score epilogue uses
 // 8 (two per quarter, split at a head boundary: its per-row score chains are
 // the long pole there)
-template <bool SC>
-constexpr int nepi() { return SC ? 8 : 4; }
-template <bool SC>
-constexpr int threads3() { return (W_EPI + nepi<SC>()) * 32; }
+// epilogue warps: the score-fused BN = 256 tiles drain faster with 8 (100 -> 4x64:
+// 0.93 vs 1.07 ms); at BN = 192 four keep a 4th operand stage (256 -> 4x47: 1.21
+// vs 1.30 ms; profiles/r02c_gemm_sc_epi_warps.jsonl)
+template <int BN, bool SC>
+constexpr int nepi() { return SC && BN == 256 ? 8 : 4; }
+template <int BN, bool SC>
+constexpr int threads3() { return (W_EPI + nepi<BN, SC>()) * 32; }
 constexpr int RL = 2;                       // A lo ring depth (shared memory, pair kernels)
 constexpr int RT = 4;                       // A hi/lo TMEM slots (resident-W kernels)
 constexpr uint32_t TS_BASE = 256;           // first TMEM column of the A slots
@@ -1146,7 +1149,7 @@ template <int BN, bool SC>
 constexpr int epi_bytes() {
   // two score tables (a_src | a_dst): at BN = 256 this keeps the epilogue at 48 KB,
   // so the score-fused pair kernel holds 3 operand stages like the plain one
-  return nepi<SC>() * (32 * EPI_LD + BN) * 4 + (SC ? 2 * v2::kScMaxN * 4 : 0);
+  return nepi<BN, SC>() * (32 * EPI_LD + BN) * 4 + (SC ? 2 * v2::kScMaxN * 4 : 0);
 }
 
 template <int BN, bool PAIR, bool RESW, bool SC>
@@ -1329,11 +1332,11 @@ struct V3Args {
 };
 
 template <int BN, int ACT, bool SC, bool PAIR, bool RESW>
-__global__ void __launch_bounds__(threads3<SC>(), 1)
+__global__ void __launch_bounds__(threads3<BN, SC>(), 1)
 gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                TcArgs a, V3Args g) {
   using C = Cfg3<BN, PAIR>;
-  constexpr int NEPI = nepi<SC>();
+  constexpr int NEPI = nepi<BN, SC>();
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment for the 128 B swizzle atoms
   // (offset arithmetic on the __shared__ array keeps the state-space provenance,
@@ -1560,7 +1563,7 @@ gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int cbeg = 0, cend = BN;
     if constexpr (SC) {
       const int split = ((a.heads + 1) / 2) * a.head_pitch;
-      if (split % 16 == 0 && split < BN) {
+      if (NEPI == 8 && split % 16 == 0 && split < BN) {
         cbeg = p ? split : 0;
         cend = p ? BN : split;
       } else if (p) {
@@ -1720,7 +1723,7 @@ int launch_v3(TcArgs a, cudaStream_t s) {
                       : std::min<int64_t>(g.num_tiles, sms);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(ctas));
-  cfg.blockDim = dim3(threads3<SC>());
+  cfg.blockDim = dim3(threads3<BN, SC>());
   cfg.dynamicSmemBytes = static_cast<size_t>(p.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
